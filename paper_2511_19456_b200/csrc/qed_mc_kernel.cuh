@@ -1,0 +1,176 @@
+// qed_mc_kernel.cuh -- fused Monte-Carlo kernel:
+// Philox4x32-10 -> massive RAMBO (CM frame) -> |M|^2 (same eval_point as qed_eval_msq)
+// -> weight x cut -> deterministic per-chunk partial sums.  The caller all-reduces the
+// chunk vector across ranks (the only collective).
+//
+// Phase space (the paper gives none; reading R9):
+// RAMBO, Kleiss-Stirling-Ellis CPC 40 (1986) 359, rambo.f conventions:
+//   q_i: c = 2 r1 - 1, phi = 2 pi r2, q0 = -log(r3 r4), q = q0 (sqrt(1-c^2) cos phi, sqrt(1-c^2) sin phi, c)
+//   boost + scale to (sqrt s, 0); mass rescaling sum_i sqrt(m_i^2 + xi^2 p_i0^2) = sqrt s (Newton)
+//   w = (2pi)^(4-3K) (pi/2)^(K-1) s^(K-2) / ((K-1)!(K-2)!) xi^(2K-3) sqrt(s) prod(|k_i|/E_i) / sum(|k_i|^2/E_i)
+// Random numbers: Philox4x32-10 (Salmon et al., SC'11), key = seed, counter =
+// (index_lo, index_hi, particle, draw); uniform u = (53-bit integer + 0.5) 2^-53.
+#pragma once
+#include "qed_eval_kernel.cuh"
+#include "qed_mc_args.h"
+
+namespace qed {
+
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ double u53(unsigned hi, unsigned lo) {
+  const unsigned long long r = ((unsigned long long)hi << 21) | (lo >> 11);
+  return ((double)r + 0.5) * 0x1.0p-53;
+}
+
+// Massive RAMBO for K final particles (particle 0 = electron, m = 1; others massless),
+// written into mom (particle order e-_in, gamma_in, e-_out, gamma_out...); returns the weight.
+template <int K>
+__device__ double rambo_point(unsigned long long idx, const QedMcArgs& m, double* mom) {
+  const uint2 key = make_uint2((unsigned)m.seed, (unsigned)(m.seed >> 32));
+  double q[K][4];
+  double Q[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const uint4 a = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 0u), key);
+    const uint4 b = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 1u), key);
+    const double r1 = u53(a.x, a.y), r2 = u53(a.z, a.w), r3 = u53(b.x, b.y), r4 = u53(b.z, b.w);
+    const double c = 2.0 * r1 - 1.0, st = sqrt(1.0 - c * c), f = 2.0 * M_PI * r2;
+    const double q0 = -log(r3 * r4);
+    double sf, cf;
+    sincos(f, &sf, &cf);
+    q[i][0] = q0; q[i][1] = q0 * st * cf; q[i][2] = q0 * st * sf; q[i][3] = q0 * c;
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) Q[mu] += q[i][mu];
+  }
+  const double sqs = m.sqrt_s, s = sqs * sqs;
+  const double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
+  const double b1 = -Q[1] / M, b2 = -Q[2] / M, b3 = -Q[3] / M;
+  const double x = sqs / M, gam = Q[0] / M, aa = 1.0 / (1.0 + gam);
+  double p0[K], pv[K][3];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const double bq = b1 * q[i][1] + b2 * q[i][2] + b3 * q[i][3];
+    p0[i] = x * (gam * q[i][0] + bq);
+    pv[i][0] = x * (q[i][1] + b1 * q[i][0] + aa * bq * b1);
+    pv[i][1] = x * (q[i][2] + b2 * q[i][0] + aa * bq * b2);
+    pv[i][2] = x * (q[i][3] + b3 * q[i][0] + aa * bq * b3);
+  }
+  // mass rescaling (electron mass 1): Newton on xi from rambo.f's start value
+  double xi = sqrt(1.0 - 1.0 / s);
+  for (int it = 0; it < 50; ++it) {
+    double f = -sqs, df = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const double mi2 = (i == 0) ? 1.0 : 0.0;
+      const double e = sqrt(mi2 + xi * xi * p0[i] * p0[i]);
+      f += e;
+      df += xi * p0[i] * p0[i] / e;
+    }
+    const double dxi = f / df;
+    xi -= dxi;
+    if (fabs(dxi) <= 1e-15 * xi) break;
+  }
+  // final momenta and weight
+  const double kin = (s - 1.0) / (2.0 * sqs);
+  mom[0] = (s + 1.0) / (2.0 * sqs); mom[1] = 0.0; mom[2] = 0.0; mom[3] = -kin;
+  mom[4] = kin; mom[5] = 0.0; mom[6] = 0.0; mom[7] = kin;
+  double prod = 1.0, sum = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const double mi2 = (i == 0) ? 1.0 : 0.0;
+    const double kx = xi * pv[i][0], ky = xi * pv[i][1], kz = xi * pv[i][2];
+    const double E = sqrt(mi2 + xi * xi * p0[i] * p0[i]);
+    const double kk = sqrt(kx * kx + ky * ky + kz * kz);
+    double* o = mom + 8 + 4 * i;
+    o[0] = E; o[1] = kx; o[2] = ky; o[3] = kz;
+    prod *= kk / E;
+    sum += kk * kk / E;
+  }
+  // massless volume (2pi)^(4-3K) (pi/2)^(K-1) s^(K-2) / ((K-1)! (K-2)!)
+  double vol = 1.0, fk1 = 1.0, fk2 = 1.0;
+#pragma unroll
+  for (int i = 0; i < K - 1; ++i) vol *= 0.5 * M_PI;
+#pragma unroll
+  for (int i = 0; i < K - 2; ++i) vol *= s;
+#pragma unroll
+  for (int i = 2; i <= K - 1; ++i) fk1 *= i;
+#pragma unroll
+  for (int i = 2; i <= K - 2; ++i) fk2 *= i;
+  vol /= fk1 * fk2;
+  vol *= pow(2.0 * M_PI, 4.0 - 3.0 * K);
+  double xp = 1.0;
+#pragma unroll
+  for (int i = 0; i < 2 * K - 3; ++i) xp *= xi;
+  return vol * xp * sqs * prod / sum;
+}
+
+template <class T>
+__global__ void __launch_bounds__(T::WPB * 32) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int G = T::G;
+  constexpr int PPW = 32 / G;
+  constexpr int K = T::N;  // final state: electron + n photons = N particles
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int g = lane % G;
+  const int grp = lane / G;
+  double* base = smem + (warp * PPW + grp) * T::STRIDE;
+  double* red = smem + T::WPB * PPW * T::STRIDE;  // [WPB][3]
+  const unsigned long long lo_all = m.first_index, hi_all = m.first_index + m.n_points;
+  const unsigned long long c_begin = lo_all / m.chunk, c_end = (hi_all + m.chunk - 1) / m.chunk;
+  for (unsigned long long c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
+    const unsigned long long lo = max(lo_all, c * (unsigned long long)m.chunk);
+    const unsigned long long hi = min(hi_all, (c + 1) * (unsigned long long)m.chunk);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (unsigned long long p0 = lo + (unsigned long long)warp * PPW; p0 < hi; p0 += (unsigned long long)T::WPB * PPW) {
+      const unsigned long long idx = p0 + grp;
+      const bool valid = idx < hi;
+      double w = 0.0;
+      bool pass = false;
+      if (g == 0) {
+        w = rambo_point<K>(valid ? idx : hi - 1, m, base + T::MOM);
+        pass = true;
+        for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
+      }
+      __syncwarp();
+      double acc[16];
+      eval_point<T>(base, g, a, acc);
+      const double msq = group_msq<T>(acc, g, a);
+      double v = (g == 0 && valid && pass) ? w * msq : 0.0;
+      double v2 = v * v, np = (g == 0 && valid && pass) ? 1.0 : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        np += __shfl_xor_sync(0xffffffffu, np, o);
+      }
+      s0 += v; s1 += v2; s2 += np;
+    }
+    if (lane == 0) {
+      red[3 * warp] = s0; red[3 * warp + 1] = s1; red[3 * warp + 2] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      for (int w = 0; w < T::WPB; ++w) { t0 += red[3 * w]; t1 += red[3 * w + 1]; t2 += red[3 * w + 2]; }
+      m.partials[3 * c] += t0;
+      m.partials[3 * c + 1] += t1;
+      m.partials[3 * c + 2] += t2;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace qed

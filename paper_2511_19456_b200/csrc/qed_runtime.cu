@@ -1,0 +1,305 @@
+// qed_runtime.cu -- libqed C-ABI (include/qed.h): handles, argument validation,
+// launch configuration and error reporting around the generated kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "qed.h"
+#include "qed_kernel_args.h"
+#include "qed_mc_args.h"
+
+extern "C" {
+const void* qedgen_kernel_N2(int);
+const void* qedgen_kernel_N3(int);
+const void* qedgen_kernel_N4(int);
+const void* qedgen_kernel_N5(int);
+const void* qedgen_kernel_N6(int);
+const void* qedgen_mc_kernel_N2(void);
+const void* qedgen_mc_kernel_N3(void);
+const void* qedgen_mc_kernel_N4(void);
+const void* qedgen_mc_kernel_N5(void);
+const void* qedgen_mc_kernel_N6(void);
+void qedgen_config_N2(int*, int*, long long*, long long*);
+void qedgen_config_N3(int*, int*, long long*, long long*);
+void qedgen_config_N4(int*, int*, long long*, long long*);
+void qedgen_config_N5(int*, int*, long long*, long long*);
+void qedgen_config_N6(int*, int*, long long*, long long*);
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+qed_status fail(qed_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+qed_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(QED_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct KernelEntry {
+  const void* (*kernel)(int);
+  const void* (*mc_kernel)(void);
+  void (*config)(int*, int*, long long*, long long*);
+};
+
+const KernelEntry kKernels[] = {
+    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2}, {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3},
+    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4}, {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5},
+    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6},
+};
+
+}  // namespace
+
+struct qed_process {
+  int n = 0, N = 0, n_in_ph = 0, n_out_ph = 0, n_ext = 0;
+  qed::QedEvalArgs args{};
+  const void* kern[2] = {nullptr, nullptr};
+  const void* kern_mc = nullptr;
+  int wpb = 0, ppw = 0, grid_blocks = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
+  long long smem = 0, smem_mc = 0, flops = 0;
+  // staging for the host-buffer entry point
+  std::mutex mu;
+  double* d_mom = nullptr;
+  double* d_out = nullptr;
+  long long cap = 0;
+  cudaStream_t stream = nullptr;
+};
+
+extern "C" {
+
+const char* qed_last_error(void) { return g_last_error.c_str(); }
+
+int64_t qed_launch_count(void) { return g_launches.load(); }
+
+static qed_status check_spec(const qed_state_spec* s, const char* side) {
+  if (!s) return fail(QED_ERR_INVALID_ARGUMENT, std::string(side) + " spec is NULL");
+  if (s->n_photons < 0) return fail(QED_ERR_INVALID_ARGUMENT, std::string(side) + ".n_photons < 0");
+  if (s->spins)
+    for (int i = 0; i <= s->n_photons; ++i)
+      if (s->spins[i] < -1 || s->spins[i] > 1)
+        return fail(QED_ERR_INVALID_ARGUMENT, std::string(side) + ".spins entries must be -1, 0 or 1");
+  return QED_OK;
+}
+
+qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
+                              qed_process** proc) {
+  if (!proc) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
+  *proc = nullptr;
+  qed_status st;
+  if ((st = check_spec(in, "in")) != QED_OK) return st;
+  if ((st = check_spec(out, "out")) != QED_OK) return st;
+  const int N = in->n_photons + out->n_photons;
+  if (N != n_photons + 1)
+    return fail(QED_ERR_INVALID_ARGUMENT, "in.n_photons + out.n_photons must equal n_photons + 1");
+  if (n_photons < 1 || n_photons > 5)
+    return fail(QED_ERR_UNSUPPORTED, "supported photon counts: 1 <= n <= 5 (N = n+1 photons on the line)");
+
+  qed_process* P = new (std::nothrow) qed_process;
+  if (!P) return fail(QED_ERR_OUT_OF_MEMORY, "host allocation failed");
+  P->n = n_photons;
+  P->N = N;
+  P->n_in_ph = in->n_photons;
+  P->n_out_ph = out->n_photons;
+  P->n_ext = N + 2;
+
+  // particle indices: e-_in = 0, photons in 1..n_in, e-_out = n_in + 1, photons out after it
+  const int e_out = P->n_in_ph + 1;
+  auto photon_particle = [&](int i) { return i < P->n_in_ph ? 1 + i : P->n_in_ph + 2 + (i - P->n_in_ph); };
+  auto spin_of = [&](int particle) -> int {
+    if (particle <= P->n_in_ph) return in->spins ? in->spins[particle] : -1;
+    int k = particle - e_out;
+    return out->spins ? out->spins[k] : -1;
+  };
+  qed::QedEvalArgs& a = P->args;
+  a.n_in_ph = P->n_in_ph;
+  a.e_out_particle = e_out;
+  a.photon_particle = 0;
+  for (int i = 0; i < N; ++i) a.photon_particle |= (unsigned)photon_particle(i) << (4 * i);
+  // internal configuration bits: 0 = e-_in spin, 1 + i = photon i, N + 1 = e-_out spin
+  int ext_of_bit[10];
+  ext_of_bit[0] = 0;
+  for (int i = 0; i < N; ++i) ext_of_bit[1 + i] = photon_particle(i);
+  ext_of_bit[N + 1] = e_out;
+  a.ext_bit = 0;
+  a.fixed_mask = a.fixed_val = 0;
+  for (int b = 0; b < N + 2; ++b) {
+    a.ext_bit |= (unsigned long long)ext_of_bit[b] << (4 * b);
+    int sp = spin_of(ext_of_bit[b]);
+    if (sp >= 0) {
+      a.fixed_mask |= 1u << b;
+      a.fixed_val |= (unsigned)sp << b;
+    }
+  }
+  // e^(2N) and 1/2 per summed initial particle (averaging)
+  const double alpha = 1.0 / 137.035999084;
+  double norm = std::pow(4.0 * M_PI * alpha, N);
+  for (int j = 0; j <= P->n_in_ph; ++j)
+    if (spin_of(j) < 0) norm *= 0.5;
+  a.norm = norm;
+
+  const KernelEntry& ke = kKernels[N - 2];
+  P->kern[0] = ke.kernel(0);
+  P->kern[1] = ke.kernel(1);
+  ke.config(&P->wpb, &P->ppw, &P->smem, &P->flops);
+
+  cudaError_t e = cudaGetDevice(&P->device);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaGetDevice"); }
+  e = cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+  int blocks_per_sm = 1 << 30;
+  for (int v = 0; v < 2; ++v) {
+    e = cudaFuncSetAttribute(P->kern[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem);
+    if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, P->kern[v], P->wpb * 32, (size_t)P->smem);
+    if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor"); }
+    blocks_per_sm = std::min(blocks_per_sm, std::max(b, 1));
+  }
+  P->grid_blocks = blocks_per_sm * P->num_sms;
+  // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
+  P->kern_mc = ke.mc_kernel();
+  P->smem_mc = P->smem + 3LL * 8 * P->wpb;
+  e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaFuncSetAttribute(mc)"); }
+  int bmc = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bmc, P->kern_mc, P->wpb * 32, (size_t)P->smem_mc);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(mc)"); }
+  P->mc_grid_blocks = std::max(bmc, 1) * P->num_sms;
+  *proc = P;
+  return QED_OK;
+}
+
+qed_status qed_process_destroy(qed_process* proc) {
+  if (!proc) return QED_OK;
+  if (proc->d_mom) cudaFree(proc->d_mom);
+  if (proc->d_out) cudaFree(proc->d_out);
+  if (proc->stream) cudaStreamDestroy(proc->stream);
+  delete proc;
+  return QED_OK;
+}
+
+static qed_status launch_eval(const qed_process* P, const double* mom, int64_t n_points, double* out,
+                              cudaStream_t stream, int per_config) {
+  if (!P) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
+  if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
+  if (n_points == 0) return QED_OK;
+  if (!mom || !out) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
+  if (((uintptr_t)mom & 7) || ((uintptr_t)out & 7)) return fail(QED_ERR_INVALID_ARGUMENT, "pointers must be 8-byte aligned");
+  qed::QedEvalArgs a = P->args;
+  a.mom = mom;
+  a.out = out;
+  a.n_points = n_points;
+  const long long per_block = (long long)P->wpb * P->ppw;
+  const long long need = (n_points + per_block - 1) / per_block;
+  const int grid = (int)std::min<long long>(need, P->grid_blocks);
+  void* params[] = {&a};
+  cudaError_t e = cudaLaunchKernel(P->kern[per_config], dim3(grid), dim3(P->wpb * 32), params, (size_t)P->smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  g_launches.fetch_add(1);
+  return QED_OK;
+}
+
+qed_status qed_eval_msq(const qed_process* proc, const double* momenta, int64_t n_points, double* out, void* stream) {
+  return launch_eval(proc, momenta, n_points, out, (cudaStream_t)stream, 0);
+}
+
+qed_status qed_eval_msq_configs(const qed_process* proc, const double* momenta, int64_t n_points, double* out,
+                                void* stream) {
+  return launch_eval(proc, momenta, n_points, out, (cudaStream_t)stream, 1);
+}
+
+qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_host, int64_t n_points,
+                             double* out_host) {
+  qed_process* P = const_cast<qed_process*>(cproc);
+  if (!P) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
+  if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
+  if (n_points == 0) return QED_OK;
+  if (!momenta_host || !out_host) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
+  std::lock_guard<std::mutex> lock(P->mu);
+  cudaError_t e;
+  if (!P->stream) {
+    e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+  }
+  if (P->cap < n_points) {
+    if (P->d_mom) cudaFree(P->d_mom);
+    if (P->d_out) cudaFree(P->d_out);
+    P->d_mom = P->d_out = nullptr;
+    P->cap = 0;
+    e = cudaMalloc(&P->d_mom, sizeof(double) * 4 * P->n_ext * (size_t)n_points);
+    if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging momenta");
+    e = cudaMalloc(&P->d_out, sizeof(double) * (size_t)n_points);
+    if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging out");
+    P->cap = n_points;
+  }
+  e = cudaMemcpyAsync(P->d_mom, momenta_host, sizeof(double) * 4 * P->n_ext * (size_t)n_points,
+                      cudaMemcpyHostToDevice, P->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  qed_status st = launch_eval(P, P->d_mom, n_points, P->d_out, P->stream, 0);
+  if (st != QED_OK) return st;
+  e = cudaMemcpyAsync(out_host, P->d_out, sizeof(double) * (size_t)n_points, cudaMemcpyDeviceToHost, P->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  return QED_OK;
+}
+
+qed_status qed_mc_sum(const qed_process* proc, const qed_mc_config* cfg, double* partials, void* stream) {
+  if (!proc || !cfg || !partials) return fail(QED_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (proc->n_in_ph != 1) return fail(QED_ERR_UNSUPPORTED, "qed_mc_sum supports e- gamma -> e- + n gamma only");
+  if (!(cfg->sqrt_s > 1.0)) return fail(QED_ERR_INVALID_ARGUMENT, "sqrt_s must exceed m_e");
+  if (!(cfg->omega_min >= 0.0)) return fail(QED_ERR_INVALID_ARGUMENT, "omega_min must be >= 0");
+  if (cfg->n_points == 0) return QED_OK;
+  if ((uintptr_t)partials & 7) return fail(QED_ERR_INVALID_ARGUMENT, "partials must be 8-byte aligned");
+  qed::QedEvalArgs a = proc->args;
+  a.mom = nullptr;
+  a.out = nullptr;
+  a.n_points = 0;
+  qed::QedMcArgs m;
+  m.sqrt_s = cfg->sqrt_s;
+  m.omega_min = cfg->omega_min;
+  m.seed = cfg->seed;
+  m.first_index = cfg->first_index;
+  m.n_points = cfg->n_points;
+  m.partials = partials;
+  m.chunk = QED_MC_CHUNK;
+  const unsigned long long c0 = cfg->first_index / QED_MC_CHUNK;
+  const unsigned long long c1 = (cfg->first_index + cfg->n_points + QED_MC_CHUNK - 1) / QED_MC_CHUNK;
+  const int grid = (int)std::min<unsigned long long>(c1 - c0, (unsigned long long)proc->mc_grid_blocks);
+  void* params[] = {&a, &m};
+  cudaError_t e = cudaLaunchKernel(proc->kern_mc, dim3(grid), dim3(proc->wpb * 32), params, (size_t)proc->smem_mc,
+                                   (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mc kernel launch");
+  g_launches.fetch_add(1);
+  return QED_OK;
+}
+
+qed_status qed_get_process_info(const qed_process* P, qed_process_info* info) {
+  if (!P || !info) return fail(QED_ERR_INVALID_ARGUMENT, "NULL argument");
+  info->n_photons = P->n;
+  info->n_ext = P->n_ext;
+  info->n_configs = 1 << P->n_ext;
+  long long f = 1;
+  for (int i = 2; i <= P->N; ++i) f *= i;
+  info->n_diagrams = (int)f;
+  info->lanes_per_point = 32 / P->ppw;
+  info->warps_per_block = P->wpb;
+  info->smem_per_block = P->smem;
+  info->grid_blocks = P->grid_blocks;
+  info->flops_per_point = P->flops;
+  info->bytes_per_point = 8LL * (4 * P->n_ext + 1);
+  return QED_OK;
+}
+
+}  // extern "C"

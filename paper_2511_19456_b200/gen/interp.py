@@ -1,0 +1,127 @@
+"""Reference interpreter of a lowered Plan (build-time check of the generator).
+
+Executes the generated task tables on a flat per-point "shared memory" array
+with exactly the offsets the CUDA kernel uses, so a wrong table entry fails
+here (tests/test_generator.py compares it with the oracle) before any GPU
+run.  It mirrors the device arithmetic of csrc/qed_device.cuh in numpy; it is
+part of the generator's test surface, not of the product path.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .lower import Plan
+
+ALPHA = 1 / 137.035999084
+
+
+def _eslash_col(e, v):
+    e1, e2, e3 = e
+    a, b, c, d = v
+    return np.array([-(e3 * c + (e1 - 1j * e2) * d), -((e1 + 1j * e2) * c - e3 * d),
+                     e3 * a + (e1 - 1j * e2) * b, (e1 + 1j * e2) * a - e3 * b])
+
+
+def _eslash_row(e, v):
+    e1, e2, e3 = e
+    a, b, c, d = v
+    return np.array([c * e3 + d * (e1 + 1j * e2), c * (e1 - 1j * e2) - d * e3,
+                     -(a * e3 + b * (e1 + 1j * e2)), -(a * (e1 - 1j * e2) - b * e3)])
+
+
+def _prop_col(mk, v):
+    qp, qm, qx, qy, qz = mk[:5]
+    a, b, c, d = v
+    Kc = (qz * c + (qx - 1j * qy) * d, (qx + 1j * qy) * c - qz * d)
+    Ka = (qz * a + (qx - 1j * qy) * b, (qx + 1j * qy) * a - qz * b)
+    return np.array([qp * a - Kc[0], qp * b - Kc[1], Ka[0] + qm * c, Ka[1] + qm * d])
+
+
+def _prop_row(mk, v):
+    qp, qm, qx, qy, qz = mk[:5]
+    a, b, c, d = v
+    # (t, b) [[Qp, -K], [K, Qm]] = (Qp t + bK, -tK + Qm b); (x, y)K = (x qz + y(qx+iqy), x(qx-iqy) - y qz)
+    bK = (c * qz + d * (qx + 1j * qy), c * (qx - 1j * qy) - d * qz)
+    tK = (a * qz + b * (qx + 1j * qy), a * (qx - 1j * qy) - b * qz)
+    return np.array([qp * a + bK[0], qp * b + bK[1], -tK[0] + qm * c, -tK[1] + qm * d])
+
+
+def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
+    """All helicity amplitudes (external bit order, with e^N) at one point, via the tables."""
+    N, L = plan.N, plan.layout
+    sm = np.zeros(plan.stride, dtype=complex)   # complex slots; spinor = 4 entries at off/2
+    real = np.zeros(plan.stride)
+
+    def put_spinor(off, v):
+        sm[off // 2: off // 2 + 4] = v
+
+    def get_spinor(off):
+        return sm[off // 2: off // 2 + 4].copy()
+
+    photon_particle = [1 + i if i < n_in_ph else n_in_ph + 2 + (i - n_in_ph) for i in range(N)]
+    sign = [1.0 if i < n_in_ph else -1.0 for i in range(N)]
+    p, pp = mom[0], mom[n_in_ph + 1]
+    for i in range(N):
+        k = mom[photon_particle[i]]
+        kperp = math.hypot(k[1], k[2])
+        kn = math.sqrt(kperp * kperp + k[3] * k[3])
+        ct, st = k[3] / kn, kperp / kn
+        cf, sf = (k[1] / kperp, k[2] / kperp) if kperp > 0 else (1.0, 0.0)
+        real[L["EPS"] + i * 8: L["EPS"] + i * 8 + 3] = (ct * cf, ct * sf, -st)
+        real[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
+    n = math.sqrt(p[0] + 1)
+    put_spinor(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
+    put_spinor(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
+    n = math.sqrt(pp[0] + 1)
+    put_spinor(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
+    put_spinor(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
+    for m in range(1, (1 << N) - 1):
+        Q = p.copy()
+        for i in range(N):
+            if m >> i & 1:
+                Q = Q + sign[i] * mom[photon_particle[i]]
+        inv = 1 / (Q[0] ** 2 - Q[1] ** 2 - Q[2] ** 2 - Q[3] ** 2 - 1)
+        real[L["MASK"] + m * 6: L["MASK"] + m * 6 + 5] = ((Q[0] + 1) * inv, (1 - Q[0]) * inv,
+                                                          Q[1] * inv, Q[2] * inv, Q[3] * inv)
+
+    def eps(off):
+        return real[off: off + 3]
+
+    def mask(off):
+        return real[off: off + 5]
+
+    for tasks in plan.in_levels:
+        for par, e, mk, out in tasks:
+            put_spinor(out, _prop_col(mask(mk), _eslash_col(eps(e), get_spinor(par))))
+    for tasks in plan.out_levels:
+        for par, e, mk, out in tasks:
+            put_spinor(out, _prop_row(mask(mk), _eslash_row(eps(e), get_spinor(par))))
+    H = plan.H
+    amp = np.zeros(H, dtype=complex)      # internal index: s | lam_i << (1+i) | s' << (N+1)
+    for si, A in enumerate(plan.sets):
+        for par, e, mk, out in plan.set_phi_tasks[si]:
+            put_spinor(out, _prop_col(mask(mk), _eslash_col(eps(e), get_spinor(par))))
+        for par, e, mk, out in plan.set_ub_tasks[si]:
+            put_spinor(out, _eslash_row(eps(e), get_spinor(par)))
+        Ac = [x for x in range(N) if x not in A]
+        pos = plan.set_pos[si]
+        for h in range(H):
+            s, sp = h & 1, (h >> (N + 1)) & 1
+            hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
+            ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
+            for a in range(plan.n_sigma):
+                phi = get_spinor(L["PHI"] + (a * plan.n_hi + hi) * 8)
+                for b in range(plan.n_tau):
+                    ub = get_spinor(L["UBL"] + (b * plan.n_ho + ho) * 8)
+                    amp[h] += ub @ phi
+    e_n = math.sqrt(4 * math.pi * ALPHA) ** N
+    out = np.zeros(H, dtype=complex)
+    e_out = n_in_ph + 1
+    for h in range(H):
+        hx = (h & 1) | (((h >> (N + 1)) & 1) << e_out)
+        for i in range(N):
+            hx |= ((h >> (1 + i)) & 1) << photon_particle[i]
+        out[hx] = e_n * amp[h]
+    return out

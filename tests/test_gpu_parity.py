@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Tolerance (BASELINE.json north_star): relative error <= 1e-10 in FP64 on the
+summed/averaged |M|^2 per point; per configuration, |gpu - oracle| <= 1e-10 x the
+largest configuration of that point.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+# oracle-sized parity batches: several tiles (points per block) and a ragged tail
+PARITY_POINTS = {1: 4099, 2: 4099, 3: 2053, 4: 259, 5: 67}
+
+
+@pytest.fixture(scope="module")
+def qed():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_19456_b200 import qed as q
+    return q
+
+
+def _gpu_msq(qed, proc, mom_aos: torch.Tensor) -> np.ndarray:
+    soa = synthetic.to_soa(mom_aos).cuda()
+    out = torch.full((mom_aos.shape[0],), float("nan"), dtype=torch.float64, device="cuda")
+    proc.eval_msq(soa, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _gpu_configs(qed, proc, mom_aos: torch.Tensor) -> np.ndarray:
+    n = mom_aos.shape[0]
+    soa = synthetic.to_soa(mom_aos).cuda()
+    out = torch.full((n * (1 << proc.n_ext),), float("nan"), dtype=torch.float64, device="cuda")
+    proc.eval_msq_configs(soa, out, n)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().reshape(n, -1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_averaged_msq_matches_oracle(qed, n):
+    mom = synthetic.rambo_cm(n, PARITY_POINTS[n], sqrt_s=5.0, seed=1000 + n)
+    proc = qed.Process(n)
+    got = _gpu_msq(qed, proc, mom)
+    ref = oracle.msq(1, n, mom.numpy())
+    rel = np.abs(got / ref - 1)
+    assert np.all(np.isfinite(got))
+    assert rel.max() <= TOL, (rel.max(), int(rel.argmax()))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_per_configuration_matches_oracle(qed, n):
+    npts = min(PARITY_POINTS[n], 515)
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=2000 + n)
+    proc = qed.Process(n)
+    got = _gpu_configs(qed, proc, mom)
+    A = oracle.amps(1, n, mom.numpy())
+    ref = np.abs(A) ** 2
+    err = np.abs(got - ref) / ref.max(axis=1, keepdims=True)
+    assert err.max() <= TOL, err.max()
+
+
+def test_compton_lab_klein_nishina_config(qed):
+    """BASELINE.json configs[0]: n = 1, 4096 lab-frame points, averaged and the four
+    fixed photon-polarisation pairs (electron spins summed) vs the oracle."""
+    mom = synthetic.compton_lab(4096, seed=1)
+    ref = oracle.msq(1, 1, mom.numpy())
+    got = _gpu_msq(qed, qed.Process(1), mom)
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+    for lam in (0, 1):
+        for lamp in (0, 1):
+            proc = qed.Process(1, in_spins=[-1, lam], out_spins=[-1, lamp])
+            got = _gpu_msq(qed, proc, mom)
+            ref = oracle.msq(1, 1, mom.numpy(), spec=[-1, lam, -1, lamp])
+            assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_fixed_states_match_oracle(qed, n):
+    mom = synthetic.rambo_cm(n, 301, seed=3000 + n)
+    rng = np.random.default_rng(n)
+    for _ in range(3):
+        spec = [int(x) for x in rng.integers(-1, 2, size=n + 3)]
+        proc = qed.Process(n, in_spins=spec[:2], out_spins=spec[2:])
+        got = _gpu_msq(qed, proc, mom)
+        ref = oracle.msq(1, n, mom.numpy(), spec=spec)
+        scale = oracle.msq(1, n, mom.numpy())
+        assert np.max(np.abs(got - ref) / scale) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_paper_direction_matches_oracle(qed, n):
+    """e- gamma^n -> e- gamma: n incoming photons.  Kinematics from
+    RAMBO for the north-star process with the photon roles crossed is not physical, so
+    build it directly: RAMBO 2 -> (e + gamma) final state from an initial e- + n gamma
+    system generated as the 'final' state of a north-star point, reversed."""
+    mom = synthetic.rambo_cm(n, 257, sqrt_s=5.0, seed=4000 + n).numpy()
+    # time-reverse the north-star kinematics: initial <-> final (momenta unchanged)
+    # north-star order: e_in, g_in, e_out, g_out*n  ->  paper order: e_in', g_in'*n, e_out', g_out'
+    rev = np.concatenate([mom[:, 2:3], mom[:, 3:], mom[:, 0:1], mom[:, 1:2]], axis=1)
+    proc = qed.Process(n, n_in_photons=n)
+    got = _gpu_msq(qed, proc, torch.from_numpy(rev))
+    ref = oracle.msq(n, 1, rev)
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+def test_empty_and_single_point(qed):
+    proc = qed.Process(2)
+    soa = torch.zeros((4 * 5, 1), dtype=torch.float64, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    proc.eval_msq(soa, out, n_points=0)
+    torch.cuda.synchronize()
+    mom = synthetic.rambo_cm(2, 1, seed=5)
+    got = _gpu_msq(qed, proc, mom)
+    ref = oracle.msq(1, 2, mom.numpy())
+    assert abs(got[0] / ref[0] - 1) <= TOL
+
+
+@pytest.mark.parametrize("npts", [1, 2, 3, 5, 7, 31, 33, 63, 65, 127, 129])
+def test_ragged_sizes_n2(qed, npts):
+    proc = qed.Process(2)
+    mom = synthetic.rambo_cm(2, npts, seed=6000 + npts)
+    got = _gpu_msq(qed, proc, mom)
+    assert np.max(np.abs(got / oracle.msq(1, 2, mom.numpy()) - 1)) <= TOL
+
+
+@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 2048), (3, 1 << 20, 512), (5, 1 << 16, 24)])
+def test_full_size_sampled(qed, n, npts, sample):
+    """Bench-sized batches (the launch configuration bench.py times): sampled outputs vs the oracle."""
+    torch.manual_seed(0)
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=7000 + n, device="cuda")
+    soa = synthetic.to_soa(mom)
+    out = torch.empty(npts, dtype=torch.float64, device="cuda")
+    proc = qed.Process(n)
+    proc.eval_msq(soa, out)
+    torch.cuda.synchronize()
+    idx = torch.cat([torch.tensor([0, npts - 1]), torch.randint(0, npts, (sample,))]).unique()
+    got = out[idx.cuda()].cpu().numpy()
+    ref = oracle.msq(1, n, mom[idx.cuda()].cpu().numpy())
+    assert np.all(np.isfinite(out.cpu().numpy()))
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+def test_abi_errors(qed):
+    with pytest.raises(qed.QedError) as e:
+        qed.Process(0)
+    assert e.value.status == 2
+    with pytest.raises(qed.QedError) as e:
+        qed.Process(6)
+    assert e.value.status == 2
+    proc = qed.Process(1)
+    st = qed.library().qed_eval_msq(proc._h, None, 5, None, None)
+    assert st == 1
+    st = qed.library().qed_eval_msq(proc._h, None, -1, None, None)
+    assert st == 1
+
+
+def test_host_entry_point(qed):
+    n = 3
+    mom = synthetic.rambo_cm(n, 1001, seed=8000)
+    soa = synthetic.to_soa(mom).pin_memory()
+    out = torch.empty(1001, dtype=torch.float64).pin_memory()
+    proc = qed.Process(n)
+    proc.eval_msq_host(soa, out, 1001)
+    ref = oracle.msq(1, n, mom.numpy())
+    assert np.max(np.abs(out.numpy() / ref - 1)) <= TOL
+
+
+def test_two_streams_two_handles(qed):
+    n = 2
+    mom = synthetic.rambo_cm(n, 20000, seed=9000)
+    soa = synthetic.to_soa(mom).cuda()
+    p1, p2 = qed.Process(n), qed.Process(n, in_spins=[0, -1])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1 = torch.empty(20000, dtype=torch.float64, device="cuda")
+    o2 = torch.empty_like(o1)
+    torch.cuda.synchronize()
+    p1.eval_msq(soa, o1, stream=s1)
+    p2.eval_msq(soa, o2, stream=s2)
+    torch.cuda.synchronize()
+    ref1 = oracle.msq(1, n, mom[:500].numpy())
+    ref2 = oracle.msq(1, n, mom[:500].numpy(), spec=[0, -1, -1, -1, -1])
+    assert np.max(np.abs(o1[:500].cpu().numpy() / ref1 - 1)) <= TOL
+    assert np.max(np.abs(o2[:500].cpu().numpy() / ref2 - 1)) <= TOL
