@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(T::WPB * 32) qed_eval_kernel(QedEvalArgs a) {
           unsigned hx = 0;
 #pragma unroll
           for (int b = 0; b < T::N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
-          a.out[pt * (1LL << (T::N + 2)) + hx] = a.norm * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+          a.out[pt * (1LL << (T::N + 2)) + hx] = a.coupling * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
         }
       }
     } else {

@@ -15,6 +15,7 @@ struct QedEvalArgs {
   unsigned fixed_mask;        // internal configuration bits fixed by the process spec
   unsigned fixed_val;
   double norm;                // e^(2N) x 1/2 per summed initial particle
+  double coupling;            // e^(2N) (per-configuration output, no averaging)
 };
 
 }  // namespace qed

@@ -144,6 +144,7 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   // e^(2N) and 1/2 per summed initial particle (averaging)
   const double alpha = 1.0 / 137.035999084;
   double norm = std::pow(4.0 * M_PI * alpha, N);
+  a.coupling = norm;
   for (int j = 0; j <= P->n_in_ph; ++j)
     if (spin_of(j) < 0) norm *= 0.5;
   a.norm = norm;
