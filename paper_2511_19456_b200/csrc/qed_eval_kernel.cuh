@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(T::WPB * 32) qed_eval_kernel(QedEvalArgs a) {
   double* base = smem + (warp * PPW + grp) * T::STRIDE;
   const long long n = a.n_points;
   const long long warps_total = (long long)gridDim.x * T::WPB;
+#pragma unroll 1
   for (long long p0 = ((long long)blockIdx.x * T::WPB + warp) * PPW; p0 < n; p0 += warps_total * PPW) {
     const long long pt = p0 + grp;
     const bool valid = pt < n;

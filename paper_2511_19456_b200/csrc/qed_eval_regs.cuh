@@ -1,0 +1,155 @@
+// qed_eval_regs.cuh -- register-resident |M|^2 kernel for small processes (N = 2, 3 photons).
+//
+// The generated body (csrc/generated/qed_regs_N{N}.cu, gen/emit_regs.py) evaluates the
+// node-reduced diagram DAG (App. C) of one phase-space point for one
+// outgoing-electron spin s' as straight-line code: two threads per point, amplitudes of the
+// 2^(N+1) configurations (s, lam_1..lam_N) accumulated in registers, the in-side leaves phi
+// exchanged between the two threads through a small shared-memory slot.  Used for n = 1, 2
+// where the group kernel (qed_eval_kernel.cuh) is bound by shared-memory traffic.
+#pragma once
+#include "qed_device.cuh"
+#include "qed_kernel_args.h"
+
+namespace qed {
+
+
+// eps(k, 1), eps(k, 2) as in external_eps, into registers
+__device__ __forceinline__ void eps_regs(const double* k, double (&e)[2][3]) {
+  const double kperp = sqrt(k[1] * k[1] + k[2] * k[2]);
+  const double kn = sqrt(kperp * kperp + k[3] * k[3]);
+  const double ct = k[3] / kn, st = kperp / kn;
+  double cf = 1.0, sf = 0.0;
+  if (kperp > 0.0) {
+    cf = k[1] / kperp;
+    sf = k[2] / kperp;
+  }
+  e[0][0] = ct * cf; e[0][1] = ct * sf; e[0][2] = -st;
+  e[1][0] = -sf; e[1][1] = cf; e[1][2] = 0.0;
+}
+
+// u(p, s) = (n chi_s, sigma.p chi_s / n), n = sqrt(E + m)
+__device__ __forceinline__ spinor u_spinor(const double* p, int s) {
+  const double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  spinor u;
+  if (s == 0) {
+    u.v[0] = {n, 0}; u.v[1] = {0, 0}; u.v[2] = {p[3] * r, 0}; u.v[3] = {p[1] * r, p[2] * r};
+  } else {
+    u.v[0] = {0, 0}; u.v[1] = {n, 0}; u.v[2] = {p[1] * r, -p[2] * r}; u.v[3] = {-p[3] * r, 0};
+  }
+  return u;
+}
+
+// ubar(p', s') = u(p', s')^dagger gamma^0
+__device__ __forceinline__ spinor ubar_spinor(const double* p, int s) {
+  const double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  spinor u;
+  if (s == 0) {
+    u.v[0] = {n, 0}; u.v[1] = {0, 0}; u.v[2] = {-p[3] * r, 0}; u.v[3] = {-p[1] * r, p[2] * r};
+  } else {
+    u.v[0] = {0, 0}; u.v[1] = {n, 0}; u.v[2] = {-p[1] * r, -p[2] * r}; u.v[3] = {p[3] * r, 0};
+  }
+  return u;
+}
+
+// propagator constants of S(Q_S) for photon subset `mask`: (Qp, Qm, qx, qy, qz, 0) -> out[6]
+template <int N>
+__device__ __forceinline__ void mask_store(const double* p, const double (&q)[N][4], int mask, double* out) {
+  double Q0 = p[0], Q1 = p[1], Q2 = p[2], Q3 = p[3];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if ((mask >> i) & 1) {
+      Q0 += q[i][0]; Q1 += q[i][1]; Q2 += q[i][2]; Q3 += q[i][3];
+    }
+  const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;
+  const double inv = 1.0 / D;
+  reinterpret_cast<double2*>(out)[0] = make_double2((Q0 + 1.0) * inv, (1.0 - Q0) * inv);
+  reinterpret_cast<double2*>(out)[1] = make_double2(Q1 * inv, Q2 * inv);
+  reinterpret_cast<double2*>(out)[2] = make_double2(Q3 * inv, 0.0);
+}
+
+
+// Shared-memory spinor load that the compiler may not hoist, merge or cache in registers:
+// the phi leaves are re-read per out-side block so that only one phi spinor is live at a time.
+__device__ __forceinline__ spinor ld_spinor_stream(const double* p) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+  spinor s;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s.v[c].r), "=d"(s.v[c].i) : "r"(addr + 16 * c));
+  return s;
+}
+
+// streamed loads of eps (3 doubles, 16-byte aligned) and propagator constants (5 doubles)
+__device__ __forceinline__ void ld_stream_eps(const double* p, double (&e)[3]) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e[0]), "=d"(e[1]) : "r"(addr));
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(e[2]) : "r"(addr + 16));
+}
+__device__ __forceinline__ void ld_stream_mask(const double* p, double (&m)[5]) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(m[0]), "=d"(m[1]) : "r"(addr));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(m[2]), "=d"(m[3]) : "r"(addr + 16));
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(m[4]) : "r"(addr + 32));
+}
+
+// acc += sum_c a[c] b[c]  (S2 join: 4 complex multiply-accumulates, 16 DFMA)
+__device__ __forceinline__ void cdot_acc(const spinor& a, const spinor& b, double& re, double& im) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    re = fma(a.v[c].r, b.v[c].r, fma(-a.v[c].i, b.v[c].i, re));
+    im = fma(a.v[c].r, b.v[c].i, fma(a.v[c].i, b.v[c].r, im));
+  }
+}
+
+template <class T, bool PER_CONFIG>
+__global__ void __launch_bounds__(T::WPB * 32) qed_regs_kernel(QedEvalArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int N = T::N;
+  constexpr int NACC = 1 << (N + 1);       // configurations (s, lam_1..lam_N) per thread
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int sp = lane & 1;
+  double* sl = smem + (warp * 16 + (lane >> 1)) * T::STRIDE;
+  const long long n = a.n_points;
+  const long long warps_total = (long long)gridDim.x * T::WPB;
+#pragma unroll 1
+  for (long long p0 = ((long long)blockIdx.x * T::WPB + warp) * 16; p0 < n; p0 += warps_total * 16) {
+    const long long pt = p0 + (lane >> 1);
+    const bool valid = pt < n;
+    const long long ptc = valid ? pt : n - 1;
+    double acc[2 * NACC];
+#pragma unroll
+    for (int i = 0; i < 2 * NACC; ++i) acc[i] = 0.0;
+    T::body(a.mom, n, ptc, sp, sl, a, acc);
+    if (PER_CONFIG) {
+      if (valid) {
+#pragma unroll
+        for (int idx = 0; idx < NACC; ++idx) {
+          const unsigned h = idx | (sp << (N + 1));
+          unsigned hx = 0;
+#pragma unroll
+          for (int b = 0; b < N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
+          a.out[pt * (1LL << (N + 2)) + hx] = a.coupling * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+        }
+      }
+    } else {
+      double sum = 0.0;
+      if (a.fixed_mask == 0) {
+#pragma unroll
+        for (int idx = 0; idx < NACC; ++idx) sum = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], sum));
+      } else {
+#pragma unroll
+        for (int idx = 0; idx < NACC; ++idx) {
+          const unsigned h = idx | (sp << (N + 1));
+          const double t = fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+          sum += ((h & a.fixed_mask) == a.fixed_val) ? t : 0.0;
+        }
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      if (valid && sp == 0) a.out[pt] = a.norm * sum;
+    }
+    __syncwarp();  // phi slot reused by the next point
+  }
+}
+
+}  // namespace qed

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -31,6 +32,10 @@ void qedgen_config_N3(int*, int*, long long*, long long*);
 void qedgen_config_N4(int*, int*, long long*, long long*);
 void qedgen_config_N5(int*, int*, long long*, long long*);
 void qedgen_config_N6(int*, int*, long long*, long long*);
+const void* qedregs_kernel_N2(int);
+const void* qedregs_kernel_N3(int);
+void qedregs_config_N2(int*, int*, long long*, long long*);
+void qedregs_config_N3(int*, int*, long long*, long long*);
 }
 
 namespace {
@@ -66,7 +71,7 @@ struct qed_process {
   qed::QedEvalArgs args{};
   const void* kern[2] = {nullptr, nullptr};
   const void* kern_mc = nullptr;
-  int wpb = 0, ppw = 0, grid_blocks = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
+  int wpb = 0, ppw = 0, grid_blocks = 0, mc_wpb = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
   long long smem = 0, smem_mc = 0, flops = 0;
   // staging for the host-buffer entry point
   std::mutex mu;
@@ -150,9 +155,22 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   a.norm = norm;
 
   const KernelEntry& ke = kKernels[N - 2];
-  P->kern[0] = ke.kernel(0);
-  P->kern[1] = ke.kernel(1);
-  ke.config(&P->wpb, &P->ppw, &P->smem, &P->flops);
+  // n = 1, 2: register-resident straight-line kernels (qed_eval_regs.cuh); n >= 3: lane-group
+  // kernels with shared-memory trie staging (qed_eval_kernel.cuh).  QED_KERNEL=group forces the latter.
+  const char* force = getenv("QED_KERNEL");
+  const bool use_regs = N <= 3 && !(force && strcmp(force, "group") == 0);
+  if (use_regs) {
+    P->kern[0] = N == 2 ? qedregs_kernel_N2(0) : qedregs_kernel_N3(0);
+    P->kern[1] = N == 2 ? qedregs_kernel_N2(1) : qedregs_kernel_N3(1);
+    (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(&P->wpb, &P->ppw, &P->smem, &P->flops);
+  } else {
+    P->kern[0] = ke.kernel(0);
+    P->kern[1] = ke.kernel(1);
+    ke.config(&P->wpb, &P->ppw, &P->smem, &P->flops);
+  }
+  int mc_wpb = 0, mc_ppw = 0;
+  long long mc_smem = 0, mc_flops = 0;
+  ke.config(&mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
 
   cudaError_t e = cudaGetDevice(&P->device);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaGetDevice"); }
@@ -170,11 +188,12 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   P->grid_blocks = blocks_per_sm * P->num_sms;
   // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
   P->kern_mc = ke.mc_kernel();
-  P->smem_mc = P->smem + 3LL * 8 * P->wpb;
+  P->mc_wpb = mc_wpb;
+  P->smem_mc = mc_smem + 3LL * 8 * mc_wpb;
   e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaFuncSetAttribute(mc)"); }
   int bmc = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bmc, P->kern_mc, P->wpb * 32, (size_t)P->smem_mc);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bmc, P->kern_mc, P->mc_wpb * 32, (size_t)P->smem_mc);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(mc)"); }
   P->mc_grid_blocks = std::max(bmc, 1) * P->num_sms;
   *proc = P;
@@ -279,7 +298,7 @@ qed_status qed_mc_sum(const qed_process* proc, const qed_mc_config* cfg, double*
   const unsigned long long c1 = (cfg->first_index + cfg->n_points + QED_MC_CHUNK - 1) / QED_MC_CHUNK;
   const int grid = (int)std::min<unsigned long long>(c1 - c0, (unsigned long long)proc->mc_grid_blocks);
   void* params[] = {&a, &m};
-  cudaError_t e = cudaLaunchKernel(proc->kern_mc, dim3(grid), dim3(proc->wpb * 32), params, (size_t)proc->smem_mc,
+  cudaError_t e = cudaLaunchKernel(proc->kern_mc, dim3(grid), dim3(proc->mc_wpb * 32), params, (size_t)proc->smem_mc,
                                    (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "mc kernel launch");
   g_launches.fetch_add(1);
