@@ -1,16 +1,14 @@
-// qed_eval_kernel.cuh -- the batched |M|^2 kernel for one process size (sm_100a, FP64 CUDA cores).
+// qed_eval_kernel.cuh -- lane-group |M|^2 kernel for one process size (sm_100a, FP64 CUDA cores).
 //
 // Instantiated once per photon count N = n+1 by the generated translation units
-// csrc/generated/qed_eval_N{N}.cu, which include the lowered node-reduction
-// fixpoint of the paper's CDAG (App. C; gen/lower.py) as task
-// tables (namespace T = qedgen_N{N}).
+// csrc/generated/qed_eval_N{N}.cu, which carry the lowered node-reduction fixpoint of the
+// paper's CDAG (App. C; gen/lower.py) as task tables and a traits struct T.
 //
-// Mapping: a group of T::G lanes evaluates one phase-space point (T::PPW = 32/G
-// points per warp, independent warps, no __syncthreads).  Lane g owns the 8
-// helicity configurations (s, lam_0, s') x fixed (lam_1..lam_{N-1}) = bits of g, and
-// accumulates their amplitudes in registers over all (n+1)! diagrams.  Shared
-// memory holds one point's external states, propagator constants, interior trie
-// nodes and the leaves of the current photon subset (layout in the tables).
+// Mapping: a group of T::G = 2^N lanes evaluates one phase-space point (a quarter, half, one or
+// two warps).  Lane g owns the 4 configurations (s, s') x (lam_i = bit i of g) and accumulates
+// their amplitudes in registers over all (n+1)! diagrams.  Shared memory holds the point's
+// external states, propagator constants, interior trie nodes and the leaves of the current
+// photon subset (layouts: gen/lower.py).  Groups of 64 lanes synchronise with a named barrier.
 //
 // Algorithmic work per point: gen/lower.py Plan.flops.
 #pragma once
@@ -18,6 +16,93 @@
 #include "qed_kernel_args.h"
 
 namespace qed {
+
+// ---- shared-memory spinor layouts (gen/lower.py aos_slot / swz)
+__device__ __forceinline__ int aos_slot(int off, int c) { return off + 2 * (c ^ ((off >> 4) & 3)); }
+__device__ __forceinline__ int swz(int h) { return (h & ~7) | ((h + (h >> 3)) & 7); }
+
+__device__ __forceinline__ spinor ld_aos(const double* base, int off) {
+  spinor s;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s.v[c] = ld2(base + aos_slot(off, c));
+  return s;
+}
+__device__ __forceinline__ void st_aos(double* base, int off, const spinor& s) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) st2(base + aos_slot(off, c), s.v[c]);
+}
+template <int NH>
+__device__ __forceinline__ void st_leaf(double* base, int region, int idx, const spinor& s) {
+  const int row = idx / NH, h = swz(idx % NH);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) st2(base + region + ((row * 4 + c) * NH + h) * 2, s.v[c]);
+}
+__device__ __forceinline__ void ld_eps(const double* p, double (&e)[3]) {
+  const double2 e01 = *reinterpret_cast<const double2*>(p);
+  e[0] = e01.x; e[1] = e01.y; e[2] = p[2];
+}
+__device__ __forceinline__ void ld_mask(const double* p, double (&m)[5]) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  m[0] = a.x; m[1] = a.y; m[2] = b.x; m[3] = b.y; m[4] = p[4];
+}
+
+// ---- task kinds (one trie node x one helicity state); descriptor = (parent, eps, mask, out)
+template <class T>
+struct Tasks {
+  // in-side V+S1 (interior): out = S(Q) epsslash parent
+  static __device__ __forceinline__ void vs_col(double* b, ushort4 t) {
+    double e[3], m[5];
+    ld_eps(b + t.y, e);
+    ld_mask(b + t.z, m);
+    st_aos(b, t.w, prop_col(m, eslash_col(e, ld_aos(b, t.x))));
+  }
+  // out-side V+S1 (interior): out = (parent epsslash) S(Q)
+  static __device__ __forceinline__ void vs_row(double* b, ushort4 t) {
+    double e[3], m[5];
+    ld_eps(b + t.y, e);
+    ld_mask(b + t.z, m);
+    st_aos(b, t.w, prop_row(m, eslash_row(e, ld_aos(b, t.x))));
+  }
+  // in-side leaf: phi = S(Q_A) epsslash parent  (V + the propagation half of S2)
+  static __device__ __forceinline__ void phi(double* b, ushort4 t) {
+    double e[3], m[5];
+    ld_eps(b + t.y, e);
+    ld_mask(b + t.z, m);
+    st_leaf<T::NHI>(b, T::PHI, t.w, prop_col(m, eslash_col(e, ld_aos(b, t.x))));
+  }
+  // out-side leaf: ubar = parent epsslash
+  static __device__ __forceinline__ void ub(double* b, ushort4 t) {
+    double e[3];
+    ld_eps(b + t.y, e);
+    st_leaf<T::NHO>(b, T::UBL, t.w, eslash_row(e, ld_aos(b, t.x)));
+  }
+};
+
+// run COUNT tasks of one kind over the G lanes of the group (compile-time trip count, descriptors
+// loaded up front so the table latency overlaps)
+template <class T, int COUNT, class F>
+__device__ __forceinline__ void run_tasks(double* base, int g, const ushort4* __restrict__ tbl, F f) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  ushort4 d[TRIPS];
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k) {
+    const int t = g + k * T::G;
+    d[k] = (t < COUNT) ? tbl[t] : make_ushort4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k)
+    if (COUNT % T::G == 0 || g + k * T::G < COUNT) f(base, d[k]);
+}
+
+template <class T>
+__device__ __forceinline__ void group_sync(int pb) {
+  if constexpr (T::G <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pb), "r"(T::G) : "memory");
+  }
+}
 
 template <class T>
 __device__ __forceinline__ void stage_externals(double* base, int g, const QedEvalArgs& a) {
@@ -27,9 +112,21 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
     if (t < N) {
       external_eps(base + T::MOM + 4 * ((a.photon_particle >> (4 * t)) & 15), base + T::EPS + 8 * t);
     } else if (t == N) {
-      external_u(base + T::MOM, base + T::U);
+      const double* p = base + T::MOM;
+      const double nn = sqrt(p[0] + 1.0), r = 1.0 / nn;
+      spinor u0, u1;   // u(p, s) = (n chi_s, sigma.p chi_s / n)
+      u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {p[3] * r, 0}; u0.v[3] = {p[1] * r, p[2] * r};
+      u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {p[1] * r, -p[2] * r}; u1.v[3] = {-p[3] * r, 0};
+      st_aos(base, T::U, u0);
+      st_aos(base, T::U + 8, u1);
     } else if (t == N + 1) {
-      external_ubar(base + T::MOM + 4 * a.e_out_particle, base + T::UB);
+      const double* p = base + T::MOM + 4 * a.e_out_particle;
+      const double nn = sqrt(p[0] + 1.0), r = 1.0 / nn;
+      spinor u0, u1;   // ubar(p', s') = u^dagger gamma^0
+      u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {-p[3] * r, 0}; u0.v[3] = {-p[1] * r, p[2] * r};
+      u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {-p[1] * r, -p[2] * r}; u1.v[3] = {p[3] * r, 0};
+      st_aos(base, T::UB, u0);
+      st_aos(base, T::UB + 8, u1);
     } else {
       // propagator constants of S(Q_S), Q_S = p + sum_{i in S} q_i, q = +k (in) / -k (out)
       const int m = t - (N + 2) + 1;
@@ -55,126 +152,144 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
   }
 }
 
-// Join of one photon subset A: acc[s | lam0 << 1 | s' << 2] += sum_{sigma, tau} ubar_tau . phi_sigma
-// XIN: photon 0 in A -> hi tile (s, lam0) x ho tile (s'); else hi tile (s) x ho tile (s', lam0).
-template <class T, bool XIN>
-__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi_base, int ho_base, double (&acc)[16]) {
-  constexpr int KH = XIN ? 4 : 2;   // hi tile
-  constexpr int KO = XIN ? 2 : 4;   // ho tile
+// Joins of one photon subset A (S2 contraction + Sum), tile (s, s') per lane:
+// acc[c & 1][s | s' << 1] += sum_{sigma, tau} ubar_tau[ho + s'] . phi_sigma[hi + s]
+// phi of one sigma stays in registers across the tau loop; loops are rolled so that ptxas
+// cannot hoist every leaf load of the subset (which spills).
+template <class T>
+__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[2][8]) {
+  const int h0 = 2 * swz(hi), h1 = 2 * swz(hi + 1), o0 = 2 * swz(ho), o1 = 2 * swz(ho + 1);
+#pragma unroll 1
+  for (int sg = 0; sg < T::NSIG; ++sg) {
+    c2 p0[4], p1[4];
+    const double* prow = base + T::PHI + sg * 4 * T::NHI * 2;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 4; ++c) {
+      p0[c] = ld2(prow + c * T::NHI * 2 + h0);
+      p1[c] = ld2(prow + c * T::NHI * 2 + h1);
+    }
+#pragma unroll 1
+    for (int tu = 0; tu < T::NTAU; ++tu) {
+      const double* urow = base + T::UBL + tu * 4 * T::NHO * 2;
+      c2 u0[4], u1[4];
 #pragma unroll
-    for (int sg = 0; sg < T::NSIG; ++sg) {
-      c2 ph[KH];
+      for (int c = 0; c < 4; ++c) {
+        u0[c] = ld2(urow + c * T::NHO * 2 + o0);
+        u1[c] = ld2(urow + c * T::NHO * 2 + o1);
+      }
 #pragma unroll
-      for (int k = 0; k < KH; ++k) ph[k] = ld2(base + T::PHI + ((sg * T::NHI + hi_base + k) * 4 + c) * 2);
-#pragma unroll
-      for (int tu = 0; tu < T::NTAU; ++tu) {
-        c2 ub[KO];
-#pragma unroll
-        for (int m = 0; m < KO; ++m) ub[m] = ld2(base + T::UBL + ((tu * T::NHO + ho_base + m) * 4 + c) * 2);
-#pragma unroll
-        for (int k = 0; k < KH; ++k) {
-#pragma unroll
-          for (int m = 0; m < KO; ++m) {
-            // config index: s | lam0 << 1 | s' << 2
-            const int idx = XIN ? (k | (m << 2)) : (k | ((m >> 1) << 1) | ((m & 1) << 2));
-            acc[2 * idx] = fma(ub[m].r, ph[k].r, fma(-ub[m].i, ph[k].i, acc[2 * idx]));
-            acc[2 * idx + 1] = fma(ub[m].r, ph[k].i, fma(ub[m].i, ph[k].r, acc[2 * idx + 1]));
-          }
-        }
+      for (int c = 0; c < 4; ++c) {
+        double* A = acc[c & 1];
+        // (s, s') = (0,0) (1,0) (0,1) (1,1)
+        A[0] = fma(u0[c].r, p0[c].r, fma(-u0[c].i, p0[c].i, A[0]));
+        A[1] = fma(u0[c].r, p0[c].i, fma(u0[c].i, p0[c].r, A[1]));
+        A[2] = fma(u0[c].r, p1[c].r, fma(-u0[c].i, p1[c].i, A[2]));
+        A[3] = fma(u0[c].r, p1[c].i, fma(u0[c].i, p1[c].r, A[3]));
+        A[4] = fma(u1[c].r, p0[c].r, fma(-u1[c].i, p0[c].i, A[4]));
+        A[5] = fma(u1[c].r, p0[c].i, fma(u1[c].i, p0[c].r, A[5]));
+        A[6] = fma(u1[c].r, p1[c].r, fma(-u1[c].i, p1[c].i, A[6]));
+        A[7] = fma(u1[c].r, p1[c].i, fma(u1[c].i, p1[c].r, A[7]));
       }
     }
   }
 }
 
-// Stages 1-3 for the point whose momenta are in base[T::MOM..]: external states,
-// propagator constants, interior trie levels, then leaves + joins per photon subset.
-// On return lane g holds the amplitudes of its 8 configurations (without e^N).
+// Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
+// amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
 template <class T>
-__device__ __forceinline__ void eval_point(double* base, int g, const QedEvalArgs& a, double (&acc)[16]) {
-  constexpr int G = T::G;
+__device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[8]) {
   stage_externals<T>(base, g, a);
-  __syncwarp();
-  T::run_interiors(base, g);
+  group_sync<T>(pb);
+  T::run_interiors(base, g, pb);
+  double acc[2][8];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  for (int i = 0; i < 8; ++i) acc[0][i] = acc[1][i] = 0.0;
+#pragma unroll 1
   for (int si = 0; si < T::NSETS; ++si) {
-    for (int t = g; t < T::NPHI; t += G) task_vs_col(base, T::phi_task(si * T::NPHI + t));
-    for (int t = g; t < T::NUB; t += G) task_v_row(base, T::ub_task(si * T::NUB + t));
-    __syncwarp();
-    int hi_base = 0, ho_base = 0;
+    T::run_set(base, g, pb, si);
+    group_sync<T>(pb);
+    int hi = 0, ho = 0;
     const unsigned inA = T::set_mask(si);
 #pragma unroll
-    for (int i = 1; i < T::N; ++i) {
-      const int lam = (g >> (i - 1)) & 1;
-      if ((inA >> i) & 1) hi_base |= lam << T::set_pos(si, i);
-      else ho_base |= lam << T::set_pos(si, i);
+    for (int i = 0; i < T::N; ++i) {
+      const int lam = (g >> i) & 1;
+      if ((inA >> i) & 1) hi |= lam << T::set_pos(si, i);
+      else ho |= lam << T::set_pos(si, i);
     }
-    if (inA & 1) join_set<T, true>(base, hi_base, ho_base, acc);
-    else join_set<T, false>(base, hi_base, ho_base, acc);
-    __syncwarp();
+    join_set<T>(base, hi, ho, acc);
+    group_sync<T>(pb);
   }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) amp[i] = acc[0][i] + acc[1][i];
 }
 
-// internal configuration index of accumulator idx of lane g: s | lam0 << 1 | g << 2 | s' << (N+1)
+// internal configuration of amplitude k of lane g: s | lam << 1 | s' << (N+1)
 template <class T>
-__device__ __forceinline__ unsigned config_of(int idx, int g) {
-  return (idx & 1) | (((idx >> 1) & 1) << 1) | ((unsigned)g << 2) | (((idx >> 2) & 1) << (T::N + 1));
+__device__ __forceinline__ unsigned config_of(int k, int g) {
+  return (k & 1) | ((unsigned)g << 1) | ((unsigned)(k >> 1) << (T::N + 1));
 }
 
-// sum over the group's configurations allowed by the spec of |amp|^2, times norm; valid in all lanes
+// sum over the group's configurations allowed by the spec of |amp|^2, times norm (valid in every
+// lane of groups of <= 32 lanes, and in every lane of 64-lane groups after the barrier exchange)
 template <class T>
-__device__ __forceinline__ double group_msq(const double (&acc)[16], int g, const QedEvalArgs& a) {
+__device__ __forceinline__ double group_msq(const double (&amp)[8], int g, int pb, double* base, const QedEvalArgs& a) {
   double sum = 0.0;
 #pragma unroll
-  for (int idx = 0; idx < 8; ++idx) {
-    const unsigned h = config_of<T>(idx, g);
-    if ((h & a.fixed_mask) == a.fixed_val) sum = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], sum));
+  for (int k = 0; k < 4; ++k) {
+    const double t = fma(amp[2 * k], amp[2 * k], amp[2 * k + 1] * amp[2 * k + 1]);
+    sum += ((config_of<T>(k, g) & a.fixed_mask) == a.fixed_val) ? t : 0.0;
   }
+  constexpr int W = T::G < 32 ? T::G : 32;
 #pragma unroll
-  for (int o = T::G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  for (int o = W / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if constexpr (T::G > 32) {
+    if ((g & 31) == 0) base[T::RED + (g >> 5)] = sum;
+    group_sync<T>(pb);
+    sum = base[T::RED] + base[T::RED + 1];
+  }
   return a.norm * sum;
 }
 
 template <class T, bool PER_CONFIG>
-__global__ void __launch_bounds__(T::WPB * 32) qed_eval_kernel(QedEvalArgs a) {
+__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_eval_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int G = T::G;
-  constexpr int PPW = 32 / G;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int g = lane % G;
-  const int grp = lane / G;
-  double* base = smem + (warp * PPW + grp) * T::STRIDE;
+  constexpr int PB = T::WPB * 32 / G;   // points per block
+  const int g = threadIdx.x % G;
+  const int pb = threadIdx.x / G;
+  double* base = smem + pb * T::STRIDE;
   const long long n = a.n_points;
-  const long long warps_total = (long long)gridDim.x * T::WPB;
+  const long long stride_pts = (long long)gridDim.x * PB;
 #pragma unroll 1
-  for (long long p0 = ((long long)blockIdx.x * T::WPB + warp) * PPW; p0 < n; p0 += warps_total * PPW) {
-    const long long pt = p0 + grp;
+  for (long long p0 = (long long)blockIdx.x * PB; p0 < n; p0 += stride_pts) {
+    const long long pt = p0 + pb;
     const bool valid = pt < n;
     const long long ptc = valid ? pt : n - 1;
-    // stage 0: momenta, SoA layout mom[(4 j + mu) n + i]
-    for (int t = g; t < 4 * (T::N + 2); t += G) base[T::MOM + t] = __ldg(a.mom + (long long)t * n + ptc);
-    __syncwarp();
-    double acc[16];
-    eval_point<T>(base, g, a, acc);
+    // stage 0: momenta, SoA layout mom[(4 j + mu) n + i]; L2 prefetch of the next batch
+    for (int t = g; t < 4 * (T::N + 2); t += G) {
+      base[T::MOM + t] = __ldg(a.mom + (long long)t * n + ptc);
+      if (pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
+    }
+    group_sync<T>(pb);
+    double amp[8];
+    eval_point<T>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
       if (valid) {
 #pragma unroll
-        for (int idx = 0; idx < 8; ++idx) {
-          const unsigned h = config_of<T>(idx, g);
+        for (int k = 0; k < 4; ++k) {
+          const unsigned h = config_of<T>(k, g);
           unsigned hx = 0;
 #pragma unroll
           for (int b = 0; b < T::N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
-          a.out[pt * (1LL << (T::N + 2)) + hx] = a.coupling * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+          a.out[pt * (1LL << (T::N + 2)) + hx] = a.coupling * fma(amp[2 * k], amp[2 * k], amp[2 * k + 1] * amp[2 * k + 1]);
         }
       }
     } else {
-      const double msq = group_msq<T>(acc, g, a);
+      const double msq = group_msq<T>(amp, g, pb, base, a);
       if (valid && g == 0) a.out[pt] = msq;
     }
+    group_sync<T>(pb);   // the slot is reused by the next point
   }
 }
 

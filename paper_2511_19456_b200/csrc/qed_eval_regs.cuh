@@ -102,7 +102,7 @@ __device__ __forceinline__ void cdot_acc(const spinor& a, const spinor& b, doubl
 }
 
 template <class T, bool PER_CONFIG>
-__global__ void __launch_bounds__(T::WPB * 32) qed_regs_kernel(QedEvalArgs a) {
+__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_regs_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int N = T::N;
   constexpr int NACC = 1 << (N + 1);       // configurations (s, lam_1..lam_N) per thread
@@ -117,6 +117,15 @@ __global__ void __launch_bounds__(T::WPB * 32) qed_regs_kernel(QedEvalArgs a) {
     const long long pt = p0 + (lane >> 1);
     const bool valid = pt < n;
     const long long ptc = valid ? pt : n - 1;
+    {
+      // L2 prefetch of this warp's next batch of momenta (one 128-byte row per lane), so the
+      // next iteration's loads do not wait on HBM latency.
+      const long long nx = p0 + warps_total * 16;
+      if (lane < 4 * (N + 2) && nx < n) {
+        const double* r = a.mom + (long long)lane * n + nx;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+      }
+    }
     double acc[2 * NACC];
 #pragma unroll
     for (int i = 0; i < 2 * NACC; ++i) acc[i] = 0.0;

@@ -117,25 +117,23 @@ __device__ double rambo_point(unsigned long long idx, const QedMcArgs& m, double
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::WPB * 32) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
+__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
   extern __shared__ __align__(16) double smem[];
   constexpr int G = T::G;
-  constexpr int PPW = 32 / G;
-  constexpr int K = T::N;  // final state: electron + n photons = N particles
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int g = lane % G;
-  const int grp = lane / G;
-  double* base = smem + (warp * PPW + grp) * T::STRIDE;
-  double* red = smem + T::WPB * PPW * T::STRIDE;  // [WPB][3]
+  constexpr int PB = T::WPB * 32 / G;     // points per block
+  constexpr int K = T::N;                 // final state: electron + n photons = N particles
+  const int g = threadIdx.x % G;
+  const int pb = threadIdx.x / G;
+  double* base = smem + pb * T::STRIDE;
+  double* red = smem + PB * T::STRIDE;    // [PB][3] block reduction scratch
   const unsigned long long lo_all = m.first_index, hi_all = m.first_index + m.n_points;
   const unsigned long long c_begin = lo_all / m.chunk, c_end = (hi_all + m.chunk - 1) / m.chunk;
   for (unsigned long long c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
     const unsigned long long lo = max(lo_all, c * (unsigned long long)m.chunk);
     const unsigned long long hi = min(hi_all, (c + 1) * (unsigned long long)m.chunk);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (unsigned long long p0 = lo + (unsigned long long)warp * PPW; p0 < hi; p0 += (unsigned long long)T::WPB * PPW) {
-      const unsigned long long idx = p0 + grp;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;  // thread 0 only: fixed summation order over the chunk
+    for (unsigned long long p0 = lo; p0 < hi; p0 += PB) {
+      const unsigned long long idx = p0 + pb;
       const bool valid = idx < hi;
       double w = 0.0;
       bool pass = false;
@@ -144,32 +142,26 @@ __global__ void __launch_bounds__(T::WPB * 32) qed_mc_kernel(QedEvalArgs a, QedM
         pass = true;
         for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
       }
-      __syncwarp();
-      double acc[16];
-      eval_point<T>(base, g, a, acc);
-      const double msq = group_msq<T>(acc, g, a);
-      double v = (g == 0 && valid && pass) ? w * msq : 0.0;
-      double v2 = v * v, np = (g == 0 && valid && pass) ? 1.0 : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v += __shfl_xor_sync(0xffffffffu, v, o);
-        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-        np += __shfl_xor_sync(0xffffffffu, np, o);
+      group_sync<T>(pb);
+      double amp[8];
+      eval_point<T>(base, g, pb, a, amp);
+      const double msq = group_msq<T>(amp, g, pb, base, a);
+      if (g == 0) {
+        const double v = (valid && pass) ? w * msq : 0.0;
+        red[3 * pb] = v;
+        red[3 * pb + 1] = v * v;
+        red[3 * pb + 2] = (valid && pass) ? 1.0 : 0.0;
       }
-      s0 += v; s1 += v2; s2 += np;
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int q = 0; q < PB; ++q) { s0 += red[3 * q]; s1 += red[3 * q + 1]; s2 += red[3 * q + 2]; }
+      __syncthreads();
     }
-    if (lane == 0) {
-      red[3 * warp] = s0; red[3 * warp + 1] = s1; red[3 * warp + 2] = s2;
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-      for (int w = 0; w < T::WPB; ++w) { t0 += red[3 * w]; t1 += red[3 * w + 1]; t2 += red[3 * w + 2]; }
-      m.partials[3 * c] += t0;
-      m.partials[3 * c + 1] += t1;
-      m.partials[3 * c + 2] += t2;
+      m.partials[3 * c] += s0;
+      m.partials[3 * c + 1] += s1;
+      m.partials[3 * c + 2] += s2;
     }
-    __syncthreads();
   }
 }
 

@@ -189,7 +189,7 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
   P->kern_mc = ke.mc_kernel();
   P->mc_wpb = mc_wpb;
-  P->smem_mc = mc_smem + 3LL * 8 * mc_wpb;
+  P->smem_mc = mc_smem + 3LL * 8 * (mc_wpb * 32 / (1 << N));
   e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaFuncSetAttribute(mc)"); }
   int bmc = 0;
@@ -220,7 +220,7 @@ static qed_status launch_eval(const qed_process* P, const double* mom, int64_t n
   a.mom = mom;
   a.out = out;
   a.n_points = n_points;
-  const long long per_block = (long long)P->wpb * P->ppw;
+  const long long per_block = P->ppw > 0 ? (long long)P->wpb * P->ppw : (long long)P->wpb * 32 / (1 << P->N);
   const long long need = (n_points + per_block - 1) / per_block;
   const int grid = (int)std::min<long long>(need, P->grid_blocks);
   void* params[] = {&a};
@@ -313,7 +313,7 @@ qed_status qed_get_process_info(const qed_process* P, qed_process_info* info) {
   long long f = 1;
   for (int i = 2; i <= P->N; ++i) f *= i;
   info->n_diagrams = (int)f;
-  info->lanes_per_point = 32 / P->ppw;
+  info->lanes_per_point = P->ppw > 0 ? 32 / P->ppw : 1 << P->N;
   info->warps_per_block = P->wpb;
   info->smem_per_block = P->smem;
   info->grid_blocks = P->grid_blocks;

@@ -164,7 +164,7 @@ def emit_regs_source(N: int) -> str:
 namespace qedregs_N{N} {{
 {emit_regs_body(N)}
 struct T {{
-  static constexpr int N = {N}, WPB = 4;
+  static constexpr int N = {N}, WPB = 2, MIN_BLOCKS = {6 if N == 3 else 8};
   static constexpr long long FLOPS_PER_POINT = {total}LL;
   static constexpr int STRIDE = {slot_layout(N)['STRIDE']};
   template <class ARGS2>

@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from .lower import Plan
+from .lower import Plan, aos_slot, swz
 
 ALPHA = 1 / 137.035999084
 
@@ -51,14 +51,25 @@ def _prop_row(mk, v):
 def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     """All helicity amplitudes (external bit order, with e^N) at one point, via the tables."""
     N, L = plan.N, plan.layout
-    sm = np.zeros(plan.stride, dtype=complex)   # complex slots; spinor = 4 entries at off/2
-    real = np.zeros(plan.stride)
+    sm = np.zeros(plan.stride + 8)            # real doubles, exactly as the device sees them
 
-    def put_spinor(off, v):
-        sm[off // 2: off // 2 + 4] = v
+    def put_aos(off, v):
+        for c in range(4):
+            o = aos_slot(off, c)
+            sm[o], sm[o + 1] = v[c].real, v[c].imag
 
-    def get_spinor(off):
-        return sm[off // 2: off // 2 + 4].copy()
+    def get_aos(off):
+        return np.array([complex(sm[aos_slot(off, c)], sm[aos_slot(off, c) + 1]) for c in range(4)])
+
+    def put_leaf(base, nh, idx, v):
+        row, h = divmod(idx, nh)
+        for c in range(4):
+            o = base + ((row * 4 + c) * nh + swz(h)) * 2
+            sm[o], sm[o + 1] = v[c].real, v[c].imag
+
+    def get_leaf(base, nh, row, h):
+        return np.array([complex(sm[base + ((row * 4 + c) * nh + swz(h)) * 2],
+                                 sm[base + ((row * 4 + c) * nh + swz(h)) * 2 + 1]) for c in range(4)])
 
     photon_particle = [1 + i if i < n_in_ph else n_in_ph + 2 + (i - n_in_ph) for i in range(N)]
     sign = [1.0 if i < n_in_ph else -1.0 for i in range(N)]
@@ -69,42 +80,50 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         kn = math.sqrt(kperp * kperp + k[3] * k[3])
         ct, st = k[3] / kn, kperp / kn
         cf, sf = (k[1] / kperp, k[2] / kperp) if kperp > 0 else (1.0, 0.0)
-        real[L["EPS"] + i * 8: L["EPS"] + i * 8 + 3] = (ct * cf, ct * sf, -st)
-        real[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
+        sm[L["EPS"] + i * 8: L["EPS"] + i * 8 + 3] = (ct * cf, ct * sf, -st)
+        sm[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
     n = math.sqrt(p[0] + 1)
-    put_spinor(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
-    put_spinor(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
+    put_aos(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
+    put_aos(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
     n = math.sqrt(pp[0] + 1)
-    put_spinor(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
-    put_spinor(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
+    put_aos(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
+    put_aos(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
     for m in range(1, (1 << N) - 1):
         Q = p.copy()
         for i in range(N):
             if m >> i & 1:
                 Q = Q + sign[i] * mom[photon_particle[i]]
         inv = 1 / (Q[0] ** 2 - Q[1] ** 2 - Q[2] ** 2 - Q[3] ** 2 - 1)
-        real[L["MASK"] + m * 6: L["MASK"] + m * 6 + 5] = ((Q[0] + 1) * inv, (1 - Q[0]) * inv,
-                                                          Q[1] * inv, Q[2] * inv, Q[3] * inv)
+        sm[L["MASK"] + m * 6: L["MASK"] + m * 6 + 5] = ((Q[0] + 1) * inv, (1 - Q[0]) * inv,
+                                                        Q[1] * inv, Q[2] * inv, Q[3] * inv)
 
     def eps(off):
-        return real[off: off + 3]
+        return sm[off: off + 3]
 
     def mask(off):
-        return real[off: off + 5]
+        return sm[off: off + 5]
+
+    def run(kind, tasks):
+        for par, e, mk, out in tasks:
+            if kind == "vs_col":
+                put_aos(out, _prop_col(mask(mk), _eslash_col(eps(e), get_aos(par))))
+            elif kind == "vs_row":
+                put_aos(out, _prop_row(mask(mk), _eslash_row(eps(e), get_aos(par))))
+            elif kind == "phi":
+                put_leaf(L["PHI"], plan.n_hi, out, _prop_col(mask(mk), _eslash_col(eps(e), get_aos(par))))
+            elif kind == "ub":
+                put_leaf(L["UBL"], plan.n_ho, out, _eslash_row(eps(e), get_aos(par)))
 
     for tasks in plan.in_levels:
-        for par, e, mk, out in tasks:
-            put_spinor(out, _prop_col(mask(mk), _eslash_col(eps(e), get_spinor(par))))
+        run("vs_col", tasks)
     for tasks in plan.out_levels:
-        for par, e, mk, out in tasks:
-            put_spinor(out, _prop_row(mask(mk), _eslash_row(eps(e), get_spinor(par))))
+        run("vs_row", tasks)
     H = plan.H
     amp = np.zeros(H, dtype=complex)      # internal index: s | lam_i << (1+i) | s' << (N+1)
     for si, A in enumerate(plan.sets):
-        for par, e, mk, out in plan.set_phi_tasks[si]:
-            put_spinor(out, _prop_col(mask(mk), _eslash_col(eps(e), get_spinor(par))))
-        for par, e, mk, out in plan.set_ub_tasks[si]:
-            put_spinor(out, _eslash_row(eps(e), get_spinor(par)))
+        for stage in plan.set_stages[si]:
+            for kind, tasks in stage:
+                run(kind, tasks)
         Ac = [x for x in range(N) if x not in A]
         pos = plan.set_pos[si]
         for h in range(H):
@@ -112,10 +131,9 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
             hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
             ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
             for a in range(plan.n_sigma):
-                phi = get_spinor(L["PHI"] + (a * plan.n_hi + hi) * 8)
+                phi = get_leaf(L["PHI"], plan.n_hi, a, hi)
                 for b in range(plan.n_tau):
-                    ub = get_spinor(L["UBL"] + (b * plan.n_ho + ho) * 8)
-                    amp[h] += ub @ phi
+                    amp[h] += get_leaf(L["UBL"], plan.n_ho, b, ho) @ phi
     e_n = math.sqrt(4 * math.pi * ALPHA) ** N
     out = np.zeros(H, dtype=complex)
     e_out = n_in_ph + 1

@@ -1,5 +1,5 @@
 """Lower the node-reduced CDAG (two-sided prefix trie) of one process size to the
-tables the sm_100a kernel executes.  Build-time only.
+tables the sm_100a lane-group kernel executes.  Build-time only.
 
 The fixpoint of node reduction (gen/dag.py, App. C) keeps one
 V node per ordered photon prefix grown from each electron end, one S1 node per
@@ -15,19 +15,23 @@ inputs"):
   join           amp[h] += ubar_tau(h_out) . phi_sigma(h_in)  for every diagram
                  (sigma, tau), set(sigma) = A, set(tau) = complement of A.
 
-Schedule (the static schedule of PAPER.md line 113, one device):
-  stage 0  load momenta of one phase-space point into shared memory
-  stage 1  external states (U): eps(k_i, lam), u(p, s), ubar(p', s'); and for
-           every proper photon subset S the propagator constants of
+Static schedule (one device), one group of G = 2^N lanes per point:
+  stage 0  momenta of the point -> shared memory
+  stage 1  external states (U) and, for every proper photon subset S, the constants of
            S(Q_S) = (Qslash_S + m)/(Q_S^2 - m^2), Q_S = p + sum_{i in S} q_i
-  stage 2  interior trie levels (fused V+S1 tasks), in-side and out-side
-  stage 3  for each subset A with |A| = j: its leaves (fused V+S tasks for phi,
-           V tasks for ubar) then the joins of all j!(N-j)! diagrams of A for
-           all 2^(N+2) configurations, accumulated in registers
+  stage 2  stored interior trie levels (fused V+S1 tasks), in-side and out-side
+  stage 3  for each subset A with |A| = j: the interior levels deeper than `store`
+           restricted to the prefixes inside A / its complement (recomputed per subset to
+           keep shared memory small), the leaves (V+S tasks for phi, V tasks for ubar),
+           then the joins of its j!(N-j)! diagrams, accumulated in registers
   stage 4  |amp|^2, sum / average over configurations, one store per point.
 
-A group of G lanes evaluates one point; lane l owns the 8 configurations with
-free bits (s, lam_0, s') and fixed lam_i = bit (i-1) of l for photons i >= 1.
+Lane g owns the 4 configurations (s, s') x fixed (lam_0..lam_{N-1}) = bits of g.
+
+Shared-memory spinor layouts (bank-conflict free for the access patterns):
+  interior / external spinors: 8 doubles, component c stored at 16-byte slot c ^ ((idx >> 1) & 3),
+      idx = spinor index = offset / 8;
+  leaves: component-major rows  [sigma][c][hi'] / [tau][c][ho'], hi' = swz(hi) (see swz()).
 """
 from __future__ import annotations
 
@@ -37,16 +41,27 @@ from dataclasses import dataclass, field
 
 from .dag import balanced_split, perm_count
 
-# flop model of the emitted device code (FMA = 2, add/mul = 1; gen/../csrc/qed_device.cuh)
+# flop model of the emitted device code (FMA = 2, add/mul = 1; csrc/qed_device.cuh)
 FLOPS = {
     "V": 40,          # epsslash psi: 8 real outputs x (1 mul + 2 fma)
     "S": 56,          # (Qslash+m)/D psi with pre-scaled constants: 8 x (1 mul + 3 fma)
     "JOIN": 32,       # 4 complex multiply-accumulates
     "ABS2": 4,        # |amp|^2 accumulated: fma + fma
-    "MASK": 20,       # Q_S (4 add), D (1 mul + 3 fma + 1 add), 1/D (1), 5 scaled constants (1 add + 5 mul ... )
+    "MASK": 20,       # Q_S (4 add), D (1 mul + 3 fma + 1 add), 1/D (1), 5 scaled constants
     "EPS": 12,        # per photon: 2 sqrt, 3 div, products (counted as 1 each)
     "SPINOR": 10,     # per electron: sqrt, div, 4 products, both spins
 }
+
+
+def swz(h: int) -> int:
+    """Leaf-row position of helicity index h: rotate each aligned group of 8 by h >> 3."""
+    return (h & ~7) | ((h + (h >> 3)) & 7)
+
+
+def aos_slot(off: int, c: int) -> int:
+    """Double offset of component c of the interior spinor starting at `off` (multiple of 8)."""
+    assert off % 8 == 0
+    return off + 2 * (c ^ ((off >> 4) & 3))
 
 
 @dataclass
@@ -54,7 +69,7 @@ class Plan:
     N: int
     j: int
     G: int
-    tile: int
+    store: int                      # interior levels <= store are stored once per point
     sets: list[tuple[int, ...]]
     sigmas: list[list[tuple[int, ...]]]
     taus: list[list[tuple[int, ...]]]
@@ -62,11 +77,11 @@ class Plan:
     stride: int
     in_levels: list[list[tuple[int, int, int, int]]] = field(default_factory=list)
     out_levels: list[list[tuple[int, int, int, int]]] = field(default_factory=list)
-    set_phi_tasks: list[list[tuple[int, int, int, int]]] = field(default_factory=list)
-    set_ub_tasks: list[list[tuple[int, int, int, int]]] = field(default_factory=list)
+    # per set: list of stages; each stage = (kind, tasks); kinds: "vs_col", "vs_row", "phi", "ub"
+    set_stages: list[list[list[tuple[str, list]]]] = field(default_factory=list)
     set_pos: list[list[int]] = field(default_factory=list)
-    set_x_in: list[int] = field(default_factory=list)
     flops: dict[str, int] = field(default_factory=dict)
+    executed_flops: dict[str, int] = field(default_factory=dict)
 
     @property
     def H(self) -> int:
@@ -93,54 +108,67 @@ class Plan:
         return sum(self.flops.values())
 
 
-def _prefixes(N: int, i: int):
-    return list(itertools.permutations(range(N), i))
+def _prefixes_in(elems, i: int):
+    return list(itertools.permutations(elems, i))
 
 
-def make_plan(N: int, j: int | None = None) -> Plan:
+def default_store(N: int, j: int) -> int:
+    """Interior levels stored per point; deeper ones are recomputed per subset when storing them
+    would exceed ~26 KB of shared memory per point (n = 5: level 2, 30 KB -> 2 x 3 KB per subset)."""
+    return 1 if N >= 6 else max(j, N - j)
+
+
+def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
     if N < 2:
         raise ValueError("need at least two photons (n >= 1)")
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
-    G = 1 << (N - 1)
-    tile = 8
-    assert G * tile == 1 << (N + 2)
+    if store is None:
+        store = default_store(N, j)
+    G = 1 << N
+    full = (1 << N) - 1
 
-    # ---------------------------------------------------------------- shared-memory layout (doubles)
     lay: dict[str, int] = {}
     off = 0
 
-    def alloc(name, size):
+    def alloc(name, size, align=2):
         nonlocal off
+        off = (off + align - 1) // align * align
         lay[name] = off
         off += size
-        off += off & 1          # keep 16-byte alignment
 
     alloc("MOM", 4 * (N + 2))
-    alloc("EPS", N * 2 * 4)          # [photon][lam][e1,e2,e3,pad]
-    alloc("U", 2 * 8)                # [s][4 complex]
-    alloc("UB", 2 * 8)               # [s'][4 complex]
+    alloc("RED", 2)                  # cross-warp reduction scratch (64-lane groups)
+    alloc("EPS", N * 2 * 4)          # [photon][lam][e1, e2, e3, pad]
     alloc("MASK", (1 << N) * 6)      # [subset][Qp, Qm, qx, qy, qz, pad]
-    in_nodes: list[dict[tuple, int]] = []
-    for i in range(1, j):
-        pre = _prefixes(N, i)
-        alloc(f"IN{i}", len(pre) * (1 << (i + 1)) * 8)
-        in_nodes.append({p: k for k, p in enumerate(pre)})
-    out_nodes: list[dict[tuple, int]] = []
-    for i in range(1, N - j):
-        pre = _prefixes(N, i)
-        alloc(f"OUT{i}", len(pre) * (1 << (i + 1)) * 8)
-        out_nodes.append({p: k for k, p in enumerate(pre)})
+    alloc("U", 2 * 8, 8)             # [s] spinor (AoS, swizzled)
+    alloc("UB", 2 * 8, 8)            # [s'] spinor
+    in_nodes: dict[int, dict[tuple, int]] = {}
+    out_nodes: dict[int, dict[tuple, int]] = {}
+    for i in range(1, min(j, store + 1)):
+        pre = _prefixes_in(range(N), i)
+        alloc(f"IN{i}", len(pre) * (1 << (i + 1)) * 8, 8)
+        in_nodes[i] = {p: k for k, p in enumerate(pre)}
+    for i in range(1, min(N - j, store + 1)):
+        pre = _prefixes_in(range(N), i)
+        alloc(f"OUT{i}", len(pre) * (1 << (i + 1)) * 8, 8)
+        out_nodes[i] = {p: k for k, p in enumerate(pre)}
+    # per-set recomputed interior levels: prefixes of length i inside a set of size j / N-j
+    set_in_nodes: dict[int, dict[tuple, int]] = {}
+    set_out_nodes: dict[int, dict[tuple, int]] = {}
+    for i in range(store + 1, j):
+        alloc(f"SIN{i}", perm_count(j, i) * (1 << (i + 1)) * 8, 8)
+    for i in range(store + 1, N - j):
+        alloc(f"SOUT{i}", perm_count(N - j, i) * (1 << (i + 1)) * 8, 8)
     n_sigma, n_tau = math.factorial(j), math.factorial(N - j)
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
-    alloc("PHI", n_sigma * n_hi * 8)
-    alloc("UBL", n_tau * n_ho * 8)
+    alloc("PHI", n_sigma * 4 * n_hi * 2, 8)
+    alloc("UBL", n_tau * 4 * n_ho * 2, 8)
     stride = off
-    # spread consecutive points of a warp over the 32 banks (LDS.128 phases of 8 lanes)
-    if stride % 16 == 0:
-        stride += 4
-    elif stride % 16 == 8:
+    # odd number of 16-byte slots per point: consecutive points of a warp start in different banks
+    stride = (stride + 1) // 2 * 2
+    if (stride // 2) % 2 == 0:
         stride += 2
     lay["STRIDE"] = stride
 
@@ -150,48 +178,44 @@ def make_plan(N: int, j: int | None = None) -> Plan:
     def mask_off(m):
         return lay["MASK"] + m * 6
 
-    full = (1 << N) - 1
-
-    def in_node_off(prefix, hidx):
-        i = len(prefix)
-        k = in_nodes[i - 1][prefix]
-        return lay[f"IN{i}"] + (k * (1 << (i + 1)) + hidx) * 8
-
-    def out_node_off(prefix, hidx):
-        i = len(prefix)
-        k = out_nodes[i - 1][prefix]
-        return lay[f"OUT{i}"] + (k * (1 << (i + 1)) + hidx) * 8
-
     def mask_of(ph):
         m = 0
         for x in ph:
             m |= 1 << x
         return m
 
-    plan = Plan(N=N, j=j, G=G, tile=tile, sets=[], sigmas=[], taus=[], layout=lay, stride=stride)
+    plan = Plan(N=N, j=j, G=G, store=store, sets=[], sigmas=[], taus=[], layout=lay, stride=stride)
 
-    # ---------------------------------------------------------------- interior trie levels (V+S1 fused)
-    # in-side node (sigma_1..sigma_i), helicity index s | lam_{sigma_1} << 1 | ... (by position)
-    for i in range(1, j):
-        tasks = []
-        for pre in _prefixes(N, i):
-            for h in range(1 << (i + 1)):
-                parent = lay["U"] + (h & 1) * 8 if i == 1 else in_node_off(pre[:-1], h & ((1 << i) - 1))
-                lam = (h >> i) & 1
-                tasks.append((parent, eps_off(pre[-1], lam), mask_off(mask_of(pre)), in_node_off(pre, h)))
-        plan.in_levels.append(tasks)
-    # out-side node (tau_1..tau_i) counted from the outgoing electron; propagator momentum
-    # Q_{all \ set(tau)} (momentum of the line = p + photons still on the in-side)
-    for i in range(1, N - j):
-        tasks = []
-        for pre in _prefixes(N, i):
-            for h in range(1 << (i + 1)):
-                parent = lay["UB"] + (h & 1) * 8 if i == 1 else out_node_off(pre[:-1], h & ((1 << i) - 1))
-                lam = (h >> i) & 1
-                tasks.append((parent, eps_off(pre[-1], lam), mask_off(full & ~mask_of(pre)), out_node_off(pre, h)))
-        plan.out_levels.append(tasks)
+    # ---------------------------------------------------------------- stored interior levels (V+S1 fused)
+    def in_off(prefix, h, set_local=None):
+        i = len(prefix)
+        if i in in_nodes:
+            return lay[f"IN{i}"] + (in_nodes[i][prefix] * (1 << (i + 1)) + h) * 8
+        return lay[f"SIN{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * 8
 
-    # ---------------------------------------------------------------- per-set leaves
+    def out_off(prefix, h, set_local=None):
+        i = len(prefix)
+        if i in out_nodes:
+            return lay[f"OUT{i}"] + (out_nodes[i][prefix] * (1 << (i + 1)) + h) * 8
+        return lay[f"SOUT{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * 8
+
+    def in_task(pre, h, local=None):
+        i = len(pre)
+        parent = lay["U"] + (h & 1) * 8 if i == 1 else in_off(pre[:-1], h & ((1 << i) - 1), local)
+        return (parent, eps_off(pre[-1], (h >> i) & 1), mask_off(mask_of(pre)), in_off(pre, h, local))
+
+    def out_task(pre, h, local=None):
+        i = len(pre)
+        parent = lay["UB"] + (h & 1) * 8 if i == 1 else out_off(pre[:-1], h & ((1 << i) - 1), local)
+        return (parent, eps_off(pre[-1], (h >> i) & 1), mask_off(full & ~mask_of(pre)), out_off(pre, h, local))
+
+    for i in sorted(in_nodes):
+        plan.in_levels.append([in_task(pre, h) for pre in _prefixes_in(range(N), i) for h in range(1 << (i + 1))])
+    for i in sorted(out_nodes):
+        plan.out_levels.append([out_task(pre, h) for pre in _prefixes_in(range(N), i) for h in range(1 << (i + 1))])
+
+    # ---------------------------------------------------------------- per-set stages
+    n_set_in_int = n_set_out_int = 0
     for A in itertools.combinations(range(N), j):
         Ac = tuple(x for x in range(N) if x not in A)
         sig = list(itertools.permutations(A))
@@ -205,32 +229,52 @@ def make_plan(N: int, j: int | None = None) -> Plan:
         for k, x in enumerate(Ac):
             pos[x] = 1 + k
         plan.set_pos.append(pos)
-        plan.set_x_in.append(1 if 0 in A else 0)
-        # phi_sigma[hi], hi = s | lam_{A sorted} (bit 1 + sorted position)
+        stages: list[list[tuple[str, list]]] = []
+        local_in: dict[tuple, int] = {}
+        local_out: dict[tuple, int] = {}
+        for i in range(store + 1, max(j, N - j)):
+            st = []
+            if i < j:
+                pres = _prefixes_in(A, i)
+                for k, p in enumerate(pres):
+                    local_in[p] = k
+                st.append(("vs_col", [in_task(p, h, local_in) for p in pres for h in range(1 << (i + 1))]))
+                n_set_in_int += len(st[-1][1])
+            if i < N - j:
+                pres = _prefixes_in(Ac, i)
+                for k, p in enumerate(pres):
+                    local_out[p] = k
+                st.append(("vs_row", [out_task(p, h, local_out) for p in pres for h in range(1 << (i + 1))]))
+                n_set_out_int += len(st[-1][1])
+            stages.append(st)
+        # leaves: phi_sigma[hi], hi = s | lam_{A sorted} << (1 + position); write index = sigma * n_hi + hi
         phi = []
         for si, sg in enumerate(sig):
             for hi in range(n_hi):
                 lam = {x: (hi >> pos[x]) & 1 for x in A}
                 hpar = (hi & 1) | sum(lam[sg[l]] << (l + 1) for l in range(j - 1))
-                parent = lay["U"] + (hi & 1) * 8 if j == 1 else in_node_off(sg[:-1], hpar)
-                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)),
-                            lay["PHI"] + (si * n_hi + hi) * 8))
+                parent = lay["U"] + (hi & 1) * 8 if j == 1 else in_off(sg[:-1], hpar, local_in)
+                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)), si * n_hi + hi))
         ub = []
+        L = N - j
         for ti, tu in enumerate(tau):
             for ho in range(n_ho):
                 lam = {x: (ho >> pos[x]) & 1 for x in Ac}
-                L = N - j
                 hpar = (ho & 1) | sum(lam[tu[l]] << (l + 1) for l in range(L - 1))
-                parent = lay["UB"] + (ho & 1) * 8 if L == 1 else out_node_off(tu[:-1], hpar)
-                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, lay["UBL"] + (ti * n_ho + ho) * 8))
-        plan.set_phi_tasks.append(phi)
-        plan.set_ub_tasks.append(ub)
+                parent = lay["UB"] + (ho & 1) * 8 if L == 1 else out_off(tu[:-1], hpar, local_out)
+                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, ti * n_ho + ho))
+        stages.append([("phi", phi), ("ub", ub)])
+        plan.set_stages.append(stages)
 
     # ---------------------------------------------------------------- algorithmic flops per point
-    n_in_int = sum(len(t) for t in plan.in_levels)
-    n_out_int = sum(len(t) for t in plan.out_levels)
-    n_phi = sum(len(t) for t in plan.set_phi_tasks)
-    n_ub = sum(len(t) for t in plan.set_ub_tasks)
+    # (the node-reduced DAG: every distinct trie node once, whether stored or recomputed)
+    def trie_count(levels):
+        return sum(perm_count(N, i) * (1 << (i + 1)) for i in levels)
+
+    n_in_int = trie_count(range(1, j))
+    n_out_int = trie_count(range(1, N - j))
+    n_phi = perm_count(N, j) * n_hi
+    n_ub = perm_count(N, N - j) * n_ho
     H = 1 << (N + 2)
     plan.flops = {
         "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
@@ -240,6 +284,12 @@ def make_plan(N: int, j: int | None = None) -> Plan:
         "join": math.factorial(N) * H * FLOPS["JOIN"],
         "msq": H * FLOPS["ABS2"],
     }
+    # executed (includes the per-set recomputation of deep interior levels)
+    n_in_exec = sum(len(t) for t in plan.in_levels) + n_set_in_int
+    n_out_exec = sum(len(t) for t in plan.out_levels) + n_set_out_int
+    plan.executed_flops = dict(plan.flops)
+    plan.executed_flops["trie_in"] = (n_in_exec + n_phi) * (FLOPS["V"] + FLOPS["S"])
+    plan.executed_flops["trie_out"] = n_out_exec * (FLOPS["V"] + FLOPS["S"]) + n_ub * FLOPS["V"]
     return plan
 
 
@@ -248,7 +298,6 @@ def trie_node_counts(plan: Plan) -> dict[str, int]:
     node-reduction fixpoint of gen/dag.py)."""
     N, j = plan.N, plan.j
     V = sum(perm_count(N, i) for i in range(1, j + 1)) + sum(perm_count(N, i) for i in range(1, N - j + 1))
-    S1 = sum(len(t) >> (i + 2) for i, t in enumerate(plan.in_levels)) + \
-        sum(len(t) >> (i + 2) for i, t in enumerate(plan.out_levels))
+    S1 = sum(perm_count(N, i) for i in range(1, j)) + sum(perm_count(N, i) for i in range(1, N - j))
     S2 = sum(len(s) * len(t) for s, t in zip(plan.sigmas, plan.taus))
     return {"V": V, "S1": S1, "S2": S2}

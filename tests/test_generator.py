@@ -1,0 +1,111 @@
+"""Build-time generator (paper_2511_19456_b200/gen): the CDAG of PAPER.md §2-3 and App. C,
+pinned by the paper's printed node counts, and the lowered kernel tables checked against the
+oracle through the table interpreter (no GPU)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synthetic
+from paper_2511_19456_b200.gen.dag import (build_unreduced, north_star, paper_process, reduced_counts_formula,
+                                           table1_closed_form)
+from paper_2511_19456_b200.gen.interp import eval_point
+from paper_2511_19456_b200.gen.lower import make_plan, trie_node_counts
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    out = []
+    for line in open(os.path.join(GOLDEN, name)):
+        line = line.split("#")[0].strip()
+        if line:
+            out.append(line.split())
+    return out
+
+
+@pytest.mark.parametrize("n,count", [(int(a), int(b)) for a, b in _golden("table1_node_counts.txt")])
+def test_table1_closed_form(n, count):
+    """nodes(n) = 3(n+3) + 2 + 2(2n+1)(n+1)! reproduces every Table 1 row."""
+    assert table1_closed_form(n) == count
+
+
+@pytest.mark.parametrize("n,count", [(int(a), int(b)) for a, b in _golden("table1_node_counts.txt")][:5])
+def test_generated_cdag_matches_table1(n, count):
+    """The generated (pre-optimisation) CDAG of e- gamma^n -> e- gamma has exactly Table 1's node count."""
+    g = build_unreduced(paper_process(n))
+    g.validate()
+    assert len(g) == count
+    # the north-star direction has the same topology
+    assert len(build_unreduced(north_star(n))) == count
+
+
+def test_n1_composition_fig5():
+    g = build_unreduced(paper_process(1))
+    c = g.counts()
+    entry = sum(1 for nd in g.nodes.values() if nd.kind == "data" and not nd.parents)
+    for kind, cnt in _golden("fig5_n1_composition.txt"):
+        got = entry if kind == "entry" else c.get(kind, 0) - (entry if kind == "data" else 0)
+        assert got == int(cnt), (kind, got)
+
+
+@pytest.mark.parametrize("n,nodes", [(1, 26), (2, 59), (3, 148), (4, 543), (5, 2234)])
+def test_node_reduction_fixpoint(n, nodes):
+    """Fixpoint of node reduction (App. C) = two-sided prefix trie
+    (SURVEY.md App. A.2); (n+1)! S2 joins survive."""
+    g = build_unreduced(north_star(n)).reduce_fixpoint()
+    g.validate()
+    assert len(g) == nodes
+    c = g.counts()
+    f = reduced_counts_formula(n + 1, (n + 1) // 2)
+    for k in ("V", "S1", "S2", "U", "Sum"):
+        assert c.get(k, 0) == f[k]
+    assert c["S2"] == math.factorial(n + 1)
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_fixpoint_is_order_independent(n):
+    """the fully reduced CDAG does not depend on the reduction order."""
+    ref = build_unreduced(north_star(n)).reduce_fixpoint().canonical()
+    for seed in range(4):
+        g = build_unreduced(north_star(n)).reduce_random_order(seed)
+        assert g.canonical() == ref
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_lowered_trie_equals_fixpoint(n):
+    plan = make_plan(n + 1)
+    g = build_unreduced(north_star(n)).reduce_fixpoint()
+    c = g.counts()
+    t = trie_node_counts(plan)
+    assert (t["V"], t["S1"], t["S2"]) == (c["V"], c.get("S1", 0), c["S2"])
+
+
+@pytest.mark.parametrize("n,npts", [(1, 3), (2, 3), (3, 2), (4, 1), (5, 1)])
+def test_tables_interpreted_match_oracle(n, npts):
+    """The kernel's task tables, executed with the kernel's shared-memory layout, give the
+    oracle's helicity amplitudes (catches any wrong offset before a GPU run)."""
+    plan = make_plan(n + 1)
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=300 + n).numpy()
+    A = oracle.amps(1, n, mom)
+    for k in range(npts):
+        B = eval_point(plan, mom[k], 1)
+        assert np.max(np.abs(A[k] - B)) <= 1e-12 * np.max(np.abs(A[k]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_tables_paper_direction(n):
+    plan = make_plan(n + 1)
+    mom = synthetic.rambo_cm(n, 1, sqrt_s=5.0, seed=400 + n).numpy()
+    rev = np.concatenate([mom[:, 2:3], mom[:, 3:], mom[:, 0:1], mom[:, 1:2]], axis=1)
+    A = oracle.amps(n, 1, rev)
+    B = eval_point(plan, rev[0], n)
+    assert np.max(np.abs(A[0] - B)) <= 1e-12 * np.max(np.abs(A[0]))
+
+
+def test_flop_counts_documented():
+    """Algorithmic flops per point (the roofline numerator) for n = 1..5."""
+    got = [make_plan(n + 1).flops_per_point for n in range(1, 6)]
+    assert got == [2260, 10672, 65884, 565672, 6212404]
