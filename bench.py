@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--no-per-n", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning sweeps)")
     return ap.parse_args()
 
 
@@ -235,6 +236,22 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- our arm
+def run_e2e(args, world, proc, soa, P) -> dict:
+    """Same metric through the public host-buffer API (qed_eval_msq_host): every step copies the
+    step's momenta H2D from pinned memory, evaluates, and copies |M|^2 back D2H."""
+    import torch
+    h_soa = soa.cpu().pin_memory()
+    h_out = torch.empty(P, dtype=torch.float64).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        proc.eval_msq_host(h_soa, h_out, P)
+    barrier(world)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        proc.eval_msq_host(h_soa, h_out, P)
+    e2e_s = max_over_ranks(world, time.perf_counter() - t)
+    return {"value": world * P * args.steps / e2e_s, "unit": UNIT,
+            "h2d_bytes_per_step": int(h_soa.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8)}
+
 def run_b200(args, world, rank, local):
     import torch
 
@@ -282,19 +299,9 @@ def run_b200(args, world, rank, local):
             achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 1e12), 4)
 
     # end-to-end through the public host API: H2D momenta + kernel + D2H |M|^2 each step
-    h_soa = soa.cpu().pin_memory()
-    h_out = torch.empty(P, dtype=torch.float64).pin_memory()
-    for _ in range(max(1, args.warmup)):
-        proc.eval_msq_host(h_soa, h_out, P)
-    barrier(world)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        proc.eval_msq_host(h_soa, h_out, P)
-    e2e_s = max_over_ranks(world, time.perf_counter() - t)
-    e2e = {"value": world * P * args.steps / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": int(h_soa.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8)}
-    del h_soa, h_out
-
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, world, proc, soa, P)
     per_n = None
     if not args.no_per_n:
         per_n = {}
@@ -330,8 +337,8 @@ def run_b200(args, world, rank, local):
                        "n": n, "global_batch": world * P, "points_per_gpu": P,
                        "parallelism": f"points sharded over {world} GPU(s), no collective",
                        "l2": "inputs > 126 MB L2 (no flush needed)",
-                       "kernel": {k: info[k] for k in ("lanes_per_point", "warps_per_block", "smem_per_block",
-                                                       "grid_blocks")}},
+                       "kernel": dict({k: info[k] for k in ("lanes_per_point", "warps_per_block", "smem_per_block",
+                                                            "grid_blocks")}, variant=os.environ.get("QED_VARIANT", "0"))},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "fp64_dfma_microbench": peak, "per_n": per_n,
         }

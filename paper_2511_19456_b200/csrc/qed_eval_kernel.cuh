@@ -156,8 +156,8 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
 // acc[c & 1][s | s' << 1] += sum_{sigma, tau} ubar_tau[ho + s'] . phi_sigma[hi + s]
 // phi of one sigma stays in registers across the tau loop; loops are rolled so that ptxas
 // cannot hoist every leaf load of the subset (which spills).
-template <class T>
-__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[2][8]) {
+template <class T, int AS>
+__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[AS][8]) {
   const int h0 = 2 * swz(hi), h1 = 2 * swz(hi + 1), o0 = 2 * swz(ho), o1 = 2 * swz(ho + 1);
 #pragma unroll 1
   for (int sg = 0; sg < T::NSIG; ++sg) {
@@ -179,7 +179,7 @@ __device__ __forceinline__ void join_set(const double* __restrict__ base, int hi
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        double* A = acc[c & 1];
+        double* A = acc[c % AS];
         // (s, s') = (0,0) (1,0) (0,1) (1,1)
         A[0] = fma(u0[c].r, p0[c].r, fma(-u0[c].i, p0[c].i, A[0]));
         A[1] = fma(u0[c].r, p0[c].i, fma(u0[c].i, p0[c].r, A[1]));
@@ -196,14 +196,16 @@ __device__ __forceinline__ void join_set(const double* __restrict__ base, int hi
 
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
-template <class T>
+template <class T, int AS = 2>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[8]) {
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
   T::run_interiors(base, g, pb);
-  double acc[2][8];
+  double acc[AS][8];   // AS independent partial sums per amplitude (ILP across the c loop)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[0][i] = acc[1][i] = 0.0;
+  for (int q = 0; q < AS; ++q)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
 #pragma unroll 1
   for (int si = 0; si < T::NSETS; ++si) {
     T::run_set(base, g, pb, si);
@@ -216,11 +218,16 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
       if ((inA >> i) & 1) hi |= lam << T::set_pos(si, i);
       else ho |= lam << T::set_pos(si, i);
     }
-    join_set<T>(base, hi, ho, acc);
+    join_set<T, AS>(base, hi, ho, acc);
     group_sync<T>(pb);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) amp[i] = acc[0][i] + acc[1][i];
+  for (int i = 0; i < 8; ++i) {
+    double s = acc[0][i];
+#pragma unroll
+    for (int q = 1; q < AS; ++q) s += acc[q][i];
+    amp[i] = s;
+  }
 }
 
 // internal configuration of amplitude k of lane g: s | lam << 1 | s' << (N+1)
@@ -250,11 +257,12 @@ __device__ __forceinline__ double group_msq(const double (&amp)[8], int g, int p
   return a.norm * sum;
 }
 
-template <class T, bool PER_CONFIG>
-__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_eval_kernel(QedEvalArgs a) {
+// V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, AS accumulator split, PF prefetch)
+template <class T, class V, bool PER_CONFIG>
+__global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int G = T::G;
-  constexpr int PB = T::WPB * 32 / G;   // points per block
+  constexpr int PB = V::WPB * 32 / G;   // points per block
   const int g = threadIdx.x % G;
   const int pb = threadIdx.x / G;
   double* base = smem + pb * T::STRIDE;
@@ -268,11 +276,11 @@ __global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_eval_kernel(Qe
     // stage 0: momenta, SoA layout mom[(4 j + mu) n + i]; L2 prefetch of the next batch
     for (int t = g; t < 4 * (T::N + 2); t += G) {
       base[T::MOM + t] = __ldg(a.mom + (long long)t * n + ptc);
-      if (pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
+      if (V::PF && pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
     }
     group_sync<T>(pb);
     double amp[8];
-    eval_point<T>(base, g, pb, a, amp);
+    eval_point<T, V::AS>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
       if (valid) {

@@ -101,8 +101,9 @@ __device__ __forceinline__ void cdot_acc(const spinor& a, const spinor& b, doubl
   }
 }
 
-template <class T, bool PER_CONFIG>
-__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_regs_kernel(QedEvalArgs a) {
+// V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, PF L2 prefetch)
+template <class T, class V, bool PER_CONFIG>
+__global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int N = T::N;
   constexpr int NACC = 1 << (N + 1);       // configurations (s, lam_1..lam_N) per thread
@@ -111,9 +112,9 @@ __global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_regs_kernel(Qe
   const int sp = lane & 1;
   double* sl = smem + (warp * 16 + (lane >> 1)) * T::STRIDE;
   const long long n = a.n_points;
-  const long long warps_total = (long long)gridDim.x * T::WPB;
+  const long long warps_total = (long long)gridDim.x * V::WPB;
 #pragma unroll 1
-  for (long long p0 = ((long long)blockIdx.x * T::WPB + warp) * 16; p0 < n; p0 += warps_total * 16) {
+  for (long long p0 = ((long long)blockIdx.x * V::WPB + warp) * 16; p0 < n; p0 += warps_total * 16) {
     const long long pt = p0 + (lane >> 1);
     const bool valid = pt < n;
     const long long ptc = valid ? pt : n - 1;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_regs_kernel(Qe
       // L2 prefetch of this warp's next batch of momenta (one 128-byte row per lane), so the
       // next iteration's loads do not wait on HBM latency.
       const long long nx = p0 + warps_total * 16;
-      if (lane < 4 * (N + 2) && nx < n) {
+      if (V::PF && lane < 4 * (N + 2) && nx < n) {
         const double* r = a.mom + (long long)lane * n + nx;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
       }

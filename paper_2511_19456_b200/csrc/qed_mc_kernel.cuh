@@ -116,11 +116,11 @@ __device__ double rambo_point(unsigned long long idx, const QedMcArgs& m, double
   return vol * xp * sqs * prod / sum;
 }
 
-template <class T>
-__global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
+template <class T, class V>
+__global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
   extern __shared__ __align__(16) double smem[];
   constexpr int G = T::G;
-  constexpr int PB = T::WPB * 32 / G;     // points per block
+  constexpr int PB = V::WPB * 32 / G;     // points per block
   constexpr int K = T::N;                 // final state: electron + n photons = N particles
   const int g = threadIdx.x % G;
   const int pb = threadIdx.x / G;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(T::WPB * 32, T::MIN_BLOCKS) qed_mc_kernel(QedE
       }
       group_sync<T>(pb);
       double amp[8];
-      eval_point<T>(base, g, pb, a, amp);
+      eval_point<T, V::AS>(base, g, pb, a, amp);
       const double msq = group_msq<T>(amp, g, pb, base, a);
       if (g == 0) {
         const double v = (valid && pass) ? w * msq : 0.0;

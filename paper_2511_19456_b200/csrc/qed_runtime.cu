@@ -17,25 +17,32 @@
 #include "qed_mc_args.h"
 
 extern "C" {
-const void* qedgen_kernel_N2(int);
-const void* qedgen_kernel_N3(int);
-const void* qedgen_kernel_N4(int);
-const void* qedgen_kernel_N5(int);
-const void* qedgen_kernel_N6(int);
-const void* qedgen_mc_kernel_N2(void);
-const void* qedgen_mc_kernel_N3(void);
-const void* qedgen_mc_kernel_N4(void);
-const void* qedgen_mc_kernel_N5(void);
-const void* qedgen_mc_kernel_N6(void);
-void qedgen_config_N2(int*, int*, long long*, long long*);
-void qedgen_config_N3(int*, int*, long long*, long long*);
-void qedgen_config_N4(int*, int*, long long*, long long*);
-void qedgen_config_N5(int*, int*, long long*, long long*);
-void qedgen_config_N6(int*, int*, long long*, long long*);
-const void* qedregs_kernel_N2(int);
-const void* qedregs_kernel_N3(int);
-void qedregs_config_N2(int*, int*, long long*, long long*);
-void qedregs_config_N3(int*, int*, long long*, long long*);
+const void* qedgen_kernel_N2(int, int);
+const void* qedgen_kernel_N3(int, int);
+const void* qedgen_kernel_N4(int, int);
+const void* qedgen_kernel_N5(int, int);
+const void* qedgen_kernel_N6(int, int);
+const void* qedgen_mc_kernel_N2(int);
+int qedgen_num_variants_N2(void);
+const void* qedgen_mc_kernel_N3(int);
+int qedgen_num_variants_N3(void);
+const void* qedgen_mc_kernel_N4(int);
+int qedgen_num_variants_N4(void);
+const void* qedgen_mc_kernel_N5(int);
+int qedgen_num_variants_N5(void);
+const void* qedgen_mc_kernel_N6(int);
+int qedgen_num_variants_N6(void);
+void qedgen_config_N2(int, int*, int*, long long*, long long*);
+void qedgen_config_N3(int, int*, int*, long long*, long long*);
+void qedgen_config_N4(int, int*, int*, long long*, long long*);
+void qedgen_config_N5(int, int*, int*, long long*, long long*);
+void qedgen_config_N6(int, int*, int*, long long*, long long*);
+const void* qedregs_kernel_N2(int, int);
+int qedregs_num_variants_N2(void);
+const void* qedregs_kernel_N3(int, int);
+int qedregs_num_variants_N3(void);
+void qedregs_config_N2(int, int*, int*, long long*, long long*);
+void qedregs_config_N3(int, int*, int*, long long*, long long*);
 }
 
 namespace {
@@ -53,16 +60,27 @@ qed_status cuda_fail(cudaError_t e, const char* what) {
 }
 
 struct KernelEntry {
-  const void* (*kernel)(int);
-  const void* (*mc_kernel)(void);
-  void (*config)(int*, int*, long long*, long long*);
+  const void* (*kernel)(int, int);
+  const void* (*mc_kernel)(int);
+  void (*config)(int, int*, int*, long long*, long long*);
+  int (*num_variants)(void);
 };
 
 const KernelEntry kKernels[] = {
-    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2}, {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3},
-    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4}, {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5},
-    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6},
+    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2, qedgen_num_variants_N2},
+    {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3, qedgen_num_variants_N3},
+    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4, qedgen_num_variants_N4},
+    {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5, qedgen_num_variants_N5},
+    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6},
 };
+
+// launch variant from QED_VARIANT (tuning experiments); 0 = default, out-of-range -> 0
+int variant_from_env(int n_variants) {
+  const char* v = getenv("QED_VARIANT");
+  if (!v) return 0;
+  int x = atoi(v);
+  return (x >= 0 && x < n_variants) ? x : 0;
+}
 
 }  // namespace
 
@@ -71,6 +89,7 @@ struct qed_process {
   qed::QedEvalArgs args{};
   const void* kern[2] = {nullptr, nullptr};
   const void* kern_mc = nullptr;
+  int variant = 0;
   int wpb = 0, ppw = 0, grid_blocks = 0, mc_wpb = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
   long long smem = 0, smem_mc = 0, flops = 0;
   // staging for the host-buffer entry point
@@ -160,17 +179,21 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   const char* force = getenv("QED_KERNEL");
   const bool use_regs = N <= 3 && !(force && strcmp(force, "group") == 0);
   if (use_regs) {
-    P->kern[0] = N == 2 ? qedregs_kernel_N2(0) : qedregs_kernel_N3(0);
-    P->kern[1] = N == 2 ? qedregs_kernel_N2(1) : qedregs_kernel_N3(1);
-    (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(&P->wpb, &P->ppw, &P->smem, &P->flops);
+    const int v = variant_from_env(N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3());
+    P->variant = v;
+    P->kern[0] = N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
+    P->kern[1] = N == 2 ? qedregs_kernel_N2(1, v) : qedregs_kernel_N3(1, v);
+    (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
   } else {
-    P->kern[0] = ke.kernel(0);
-    P->kern[1] = ke.kernel(1);
-    ke.config(&P->wpb, &P->ppw, &P->smem, &P->flops);
+    const int v = variant_from_env(ke.num_variants());
+    P->variant = v;
+    P->kern[0] = ke.kernel(0, v);
+    P->kern[1] = ke.kernel(1, v);
+    ke.config(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
   }
   int mc_wpb = 0, mc_ppw = 0;
   long long mc_smem = 0, mc_flops = 0;
-  ke.config(&mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
+  ke.config(0, &mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
 
   cudaError_t e = cudaGetDevice(&P->device);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaGetDevice"); }
@@ -187,7 +210,7 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
   }
   P->grid_blocks = blocks_per_sm * P->num_sms;
   // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
-  P->kern_mc = ke.mc_kernel();
+  P->kern_mc = ke.mc_kernel(0);
   P->mc_wpb = mc_wpb;
   P->smem_mc = mc_smem + 3LL * 8 * (mc_wpb * 32 / (1 << N));
   e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);

@@ -37,6 +37,15 @@ def choose_launch(plan: Plan) -> tuple[int, int]:
     return best[1], best[2]
 
 
+def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
+    """Launch variants compiled into the library, selected at run time with QED_VARIANT:
+    (warps per block, min resident blocks, accumulator split AS, L2 prefetch).  Variant 0 is
+    the default (chosen from measurements)."""
+    wpb, mb = choose_launch(plan)
+    mb4 = max(1, min(mb, 65536 // (152 * wpb * 32)))
+    return [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
+
+
 def _tasks(name, tasks):
     if not tasks:
         return f"__device__ const ushort4 {name}[1] = {{{{0, 0, 0, 0}}}};\n"
@@ -52,6 +61,7 @@ def emit_source(plan: Plan) -> str:
     N, L = plan.N, plan.layout
     ns = f"qedgen_N{N}"
     wpb, min_blocks = choose_launch(plan)
+    vs = variants(plan)
     # stored interior levels
     in_flat, out_flat, lines = [], [], []
     for lv in range(max(len(plan.in_levels), len(plan.out_levels))):
@@ -93,10 +103,20 @@ def emit_source(plan: Plan) -> str:
     fl = plan.flops
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     lay = ", ".join(f"{k} = {L[k]}" for k in ("MOM", "RED", "EPS", "MASK", "U", "UB", "PHI", "UBL"))
+    variant_structs = "".join(
+        f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }};\n"
+        for i, (w, m, a, p) in enumerate(vs))
+    kernel_cases = "\n".join(
+        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{i}, true>\n"
+        f"                                      : (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{i}, false>;"
+        for i in range(len(vs)))
+    mc_cases = "\n".join(
+        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{ns}::T, {ns}::V{i}>;"
+        for i in range(len(vs)))
     src = f"""// GENERATED by paper_2511_19456_b200/gen/emit.py -- do not edit.
 // Process size N = {N} photons (n = {N - 1}): {len(plan.sets)} photon subsets A (|A| = j = {plan.j}),
 // {plan.n_sigma} x {plan.n_tau} diagrams per subset, {plan.H} spin/polarisation configurations,
-// G = {plan.G} lanes per point, {wpb} warps per block, {min_blocks} blocks per SM,
+// G = {plan.G} lanes per point; launch variants (warps/block, min blocks/SM, acc split, prefetch): {vs},
 // {plan.stride * 8} B shared memory per point, interior levels <= {plan.store} stored per point.
 // Algorithmic FP64 flops per point (node-reduced, helicity-shared DAG):
 {flops_comment}
@@ -110,7 +130,7 @@ __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str,
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
 
 struct T {{
-  static constexpr int N = {N}, J = {plan.j}, G = {plan.G}, WPB = {wpb}, MIN_BLOCKS = {min_blocks};
+  static constexpr int N = {N}, J = {plan.j}, G = {plan.G};
   static constexpr int STRIDE = {plan.stride};
   static constexpr int {lay};
   static constexpr int NSIG = {plan.n_sigma}, NTAU = {plan.n_tau}, NHI = {plan.n_hi}, NHO = {plan.n_ho};
@@ -125,20 +145,28 @@ struct T {{
 {run_set}
   }}
 }};
-
+{variant_structs}
 }}  // namespace {ns}
 
 extern "C" {{
-const void* qedgen_kernel_N{N}(int per_config) {{
-  return per_config ? (const void*)qed::qed_eval_kernel<{ns}::T, true>
-                    : (const void*)qed::qed_eval_kernel<{ns}::T, false>;
+int qedgen_num_variants_N{N}(void) {{ return {len(vs)}; }}
+const void* qedgen_kernel_N{N}(int per_config, int variant) {{
+  switch (variant) {{
+{kernel_cases}
+  }}
 }}
-const void* qedgen_mc_kernel_N{N}(void) {{ return (const void*)qed::qed_mc_kernel<{ns}::T>; }}
-void qedgen_config_N{N}(int* warps_per_block, int* points_per_warp, long long* smem_per_block,
+const void* qedgen_mc_kernel_N{N}(int variant) {{
+  switch (variant) {{
+{mc_cases}
+  }}
+}}
+void qedgen_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, long long* smem_per_block,
                         long long* flops_per_point) {{
-  *warps_per_block = {ns}::T::WPB;
+  static const int wpb[{len(vs)}] = {{{", ".join(str(v[0]) for v in vs)}}};
+  const int w = wpb[variant];
+  *warps_per_block = w;
   *points_per_warp = 32 / {ns}::T::G;   // 0 when a point spans two warps
-  *smem_per_block = (long long)({ns}::T::WPB * 32 / {ns}::T::G) * {ns}::T::STRIDE * 8;
+  *smem_per_block = (long long)(w * 32 / {ns}::T::G) * {ns}::T::STRIDE * 8;
   *flops_per_point = {ns}::T::FLOPS_PER_POINT;
 }}
 }}

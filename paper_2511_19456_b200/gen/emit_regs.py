@@ -154,6 +154,15 @@ def emit_regs_source(N: int) -> str:
     fl = _flops(N)
     total = sum(fl.values())
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in fl.items())
+    vs = regs_variants(N)
+    ns = f"qedregs_N{N}"
+    variant_structs = "namespace " + ns + " {\n" + "".join(
+        f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, PF = {p}; }};\n"
+        for i, (w, m, p) in enumerate(vs)) + "}\n"
+    kernel_cases = "\n".join(
+        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::T, {ns}::V{i}, true>\n"
+        f"                                      : (const void*)qed::qed_regs_kernel<{ns}::T, {ns}::V{i}, false>;"
+        for i in range(len(vs)))
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_regs.py -- do not edit.
 // Register-resident kernel for N = {N} photons (n = {N - 1}); thread = (point, s').
 // Algorithmic FP64 flops per point:
@@ -164,7 +173,7 @@ def emit_regs_source(N: int) -> str:
 namespace qedregs_N{N} {{
 {emit_regs_body(N)}
 struct T {{
-  static constexpr int N = {N}, WPB = 2, MIN_BLOCKS = {6 if N == 3 else 8};
+  static constexpr int N = {N};
   static constexpr long long FLOPS_PER_POINT = {total}LL;
   static constexpr int STRIDE = {slot_layout(N)['STRIDE']};
   template <class ARGS2>
@@ -175,20 +184,31 @@ struct T {{
 }};
 }}  // namespace qedregs_N{N}
 
+{variant_structs}
 extern "C" {{
-const void* qedregs_kernel_N{N}(int per_config) {{
-  return per_config ? (const void*)qed::qed_regs_kernel<qedregs_N{N}::T, true>
-                    : (const void*)qed::qed_regs_kernel<qedregs_N{N}::T, false>;
+int qedregs_num_variants_N{N}(void) {{ return {len(vs)}; }}
+const void* qedregs_kernel_N{N}(int per_config, int variant) {{
+  switch (variant) {{
+{kernel_cases}
+  }}
 }}
-void qedregs_config_N{N}(int* warps_per_block, int* points_per_warp, long long* smem_per_block,
+void qedregs_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, long long* smem_per_block,
                          long long* flops_per_point) {{
-  *warps_per_block = qedregs_N{N}::T::WPB;
+  static const int wpb[{len(vs)}] = {{{", ".join(str(v[0]) for v in vs)}}};
+  *warps_per_block = wpb[variant];
   *points_per_warp = 16;
-  *smem_per_block = (long long)qedregs_N{N}::T::WPB * 16 * qedregs_N{N}::T::STRIDE * 8;
+  *smem_per_block = (long long)wpb[variant] * 16 * qedregs_N{N}::T::STRIDE * 8;
   *flops_per_point = qedregs_N{N}::T::FLOPS_PER_POINT;
 }}
 }}
 """
+
+
+def regs_variants(N: int) -> list[tuple[int, int, int]]:
+    """Launch variants (warps per block, min resident blocks, L2 prefetch), QED_VARIANT selects."""
+    if N == 3:
+        return [(2, 6, 1), (4, 1, 0), (4, 1, 1), (2, 6, 0), (2, 5, 1)]
+    return [(2, 8, 1), (4, 1, 0), (4, 1, 1), (2, 8, 0), (2, 6, 1)]
 
 
 def generate_regs(out_dir: str, Ns=(2, 3)) -> list[str]:
