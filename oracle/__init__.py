@@ -54,6 +54,13 @@ def _lib(kind: str = "f64") -> ctypes.CDLL:
             getattr(lib, f).argtypes = [dp, ctypes.c_int, dp]
             getattr(lib, f).restype = None
         lib.oracle_gammas.argtypes = [dp]
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        lib.oracle_philox4x32_10.argtypes = [u32p, u32p, u32p]
+        lib.oracle_rambo_point.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, dp]
+        lib.oracle_rambo_point.restype = ctypes.c_double
+        lib.oracle_mc_sum.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, dp, ctypes.c_int]
+        lib.oracle_mc_sum.restype = ctypes.c_int
         lib.oracle_coupling_e.restype = ctypes.c_double
         lib.oracle_real_bytes.restype = ctypes.c_int
         _loaded[kind] = lib
@@ -152,3 +159,31 @@ def gammas(kind="f64"):
 
 def coupling_e(kind="f64") -> float:
     return _lib(kind).oracle_coupling_e()
+
+
+def philox4x32_10(ctr, key, kind="f64"):
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    _lib(kind).oracle_philox4x32_10(c, k, o)
+    return list(o)
+
+
+def rambo_point(n_out_ph: int, sqrt_s: float, seed: int, index: int, kind="f64"):
+    """(momenta [n+3, 4], weight) of point `index` of the MC sequence keyed by `seed`."""
+    mom = np.empty((n_out_ph + 3) * 4)
+    w = _lib(kind).oracle_rambo_point(n_out_ph, sqrt_s, seed, index, _dp(mom))
+    return mom.reshape(n_out_ph + 3, 4), w
+
+
+def mc_sum(n_out_ph: int, sqrt_s: float, omega_min: float, seed: int, first: int, count: int,
+           chunk: int = 8192, threads: int | None = None, kind="f64") -> np.ndarray:
+    """Chunk partial sums [n_chunks, 3] = (sum w|M|^2, sum (w|M|^2)^2, n_pass), n_chunks =
+    ceil((first + count) / chunk) (chunks before `first` stay zero)."""
+    n_chunks = (first + count + chunk - 1) // chunk
+    out = np.zeros(3 * n_chunks)
+    rc = _lib(kind).oracle_mc_sum(n_out_ph, sqrt_s, omega_min, seed, first, count, chunk, _dp(out),
+                                  threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_mc_sum: bad arguments")
+    return out.reshape(n_chunks, 3)

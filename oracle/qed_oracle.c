@@ -394,3 +394,165 @@ void oracle_gammas(double* out) {
 }
 double oracle_coupling_e(void) { return (double)sqrtl(4 * (real)M_PI * ALPHA); }
 int oracle_real_bytes(void) { return (int)sizeof(real); }
+
+/* ======================================================================================
+ * Monte-Carlo cross-section oracle (the paper gives no phase-space
+ * algorithm, PAPER.md line 288 -- reading R9 in DESIGN.md).  Plain transcription of:
+ *   - Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), key = seed, counter =
+ *     (index_lo, index_hi, particle, draw); u = ((hi << 21 | lo >> 11) + 0.5) 2^-53;
+ *   - massive RAMBO (Kleiss, Stirling, Ellis, CPC 40 (1986) 359, rambo.f conventions) for
+ *     e- gamma -> e- + n gamma in the CM frame (photon along +z, electron along -z);
+ *   - weight x cut (every outgoing photon E >= omega_min) x |M|^2 (point_msq above),
+ *     summed per chunk of `chunk` consecutive global indices.
+ * ====================================================================================== */
+
+typedef struct { uint32_t v[4]; } u32x4;
+
+static u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; r++) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c.v[0];
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c.v[2];
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        u32x4 n = {{hi1 ^ c.v[1] ^ k0, lo1, hi0 ^ c.v[3] ^ k1, lo0}};
+        c = n;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+void oracle_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+    u32x4 c = {{ctr[0], ctr[1], ctr[2], ctr[3]}};
+    u32x4 r = philox4x32_10(c, key[0], key[1]);
+    for (int i = 0; i < 4; i++) out[i] = r.v[i];
+}
+
+static double u53(uint32_t hi, uint32_t lo) {
+    uint64_t r = ((uint64_t)hi << 21) | (lo >> 11);
+    return ((double)r + 0.5) * 0x1.0p-53;
+}
+
+/* One phase-space point: momenta [n+3][4] in particle order e_in, g_in, e_out, g_out...;
+   returns the RAMBO weight. */
+double oracle_rambo_point(int n_out_ph, double sqrt_s, uint64_t seed, uint64_t idx, double* mom) {
+    int K = n_out_ph + 1;
+    double s = sqrt_s * sqrt_s;
+    double q[MAX_PHOTONS + 1][4], Q[4] = {0, 0, 0, 0};
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int i = 0; i < K; i++) {
+        u32x4 ca = {{(uint32_t)idx, (uint32_t)(idx >> 32), (uint32_t)i, 0u}};
+        u32x4 cb = {{(uint32_t)idx, (uint32_t)(idx >> 32), (uint32_t)i, 1u}};
+        u32x4 a = philox4x32_10(ca, k0, k1), b = philox4x32_10(cb, k0, k1);
+        double r1 = u53(a.v[0], a.v[1]), r2 = u53(a.v[2], a.v[3]);
+        double r3 = u53(b.v[0], b.v[1]), r4 = u53(b.v[2], b.v[3]);
+        double c = 2 * r1 - 1, st = sqrt(1 - c * c), f = 2 * M_PI * r2;
+        double q0 = -log(r3 * r4);
+        q[i][0] = q0;
+        q[i][1] = q0 * st * cos(f);
+        q[i][2] = q0 * st * sin(f);
+        q[i][3] = q0 * c;
+        for (int mu = 0; mu < 4; mu++) Q[mu] += q[i][mu];
+    }
+    /* conformal transformation to total momentum (sqrt s, 0) */
+    double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
+    double b[3] = {-Q[1] / M, -Q[2] / M, -Q[3] / M};
+    double x = sqrt_s / M, gam = Q[0] / M, a = 1 / (1 + gam);
+    double p0[MAX_PHOTONS + 1], pv[MAX_PHOTONS + 1][3];
+    for (int i = 0; i < K; i++) {
+        double bq = b[0] * q[i][1] + b[1] * q[i][2] + b[2] * q[i][3];
+        p0[i] = x * (gam * q[i][0] + bq);
+        for (int l = 0; l < 3; l++) pv[i][l] = x * (q[i][1 + l] + b[l] * q[i][0] + a * bq * b[l]);
+    }
+    /* mass rescaling: sum_i sqrt(m_i^2 + xi^2 p0_i^2) = sqrt s, electron (i = 0) has m = 1 */
+    double xi = sqrt(1 - 1 / s);
+    for (int it = 0; it < 50; it++) {
+        double f = -sqrt_s, df = 0;
+        for (int i = 0; i < K; i++) {
+            double m2 = i == 0 ? 1 : 0;
+            double e = sqrt(m2 + xi * xi * p0[i] * p0[i]);
+            f += e;
+            df += xi * p0[i] * p0[i] / e;
+        }
+        double dxi = f / df;
+        xi -= dxi;
+        if (fabs(dxi) <= 1e-15 * xi) break;
+    }
+    double kin = (s - 1) / (2 * sqrt_s);
+    mom[0] = (s + 1) / (2 * sqrt_s); mom[1] = 0; mom[2] = 0; mom[3] = -kin;
+    mom[4] = kin; mom[5] = 0; mom[6] = 0; mom[7] = kin;
+    double prod = 1, sum = 0;
+    for (int i = 0; i < K; i++) {
+        double m2 = i == 0 ? 1 : 0;
+        double kx = xi * pv[i][0], ky = xi * pv[i][1], kz = xi * pv[i][2];
+        double E = sqrt(m2 + xi * xi * p0[i] * p0[i]);
+        double kk = sqrt(kx * kx + ky * ky + kz * kz);
+        double* o = mom + 8 + 4 * i;
+        o[0] = E; o[1] = kx; o[2] = ky; o[3] = kz;
+        prod *= kk / E;
+        sum += kk * kk / E;
+    }
+    /* massless volume (2pi)^(4-3K) (pi/2)^(K-1) s^(K-2) / ((K-1)! (K-2)!), times the massive factor */
+    double vol = pow(2 * M_PI, 4 - 3 * K) * pow(M_PI / 2, K - 1) * pow(s, K - 2);
+    for (int i = 2; i <= K - 1; i++) vol /= i;
+    for (int i = 2; i <= K - 2; i++) vol /= i;
+    return vol * pow(xi, 2 * K - 3) * sqrt_s * prod / sum;
+}
+
+typedef struct {
+    int n;
+    double sqrt_s, omega_min;
+    uint64_t seed, first, count;
+    int chunk;
+    double* partials;    /* [n_chunks][3] local to this job */
+    uint64_t c0;         /* first chunk index of this job */
+} mc_job_t;
+
+static void* mc_worker(void* arg) {
+    mc_job_t* J = (mc_job_t*)arg;
+    proc_t P;
+    proc_init(&P, 1, J->n);
+    int8_t spec[MAX_EXT];
+    for (int j = 0; j < P.n_ext; j++) spec[j] = -1;
+    double mom[MAX_EXT * 4];
+    for (uint64_t i = J->first; i < J->first + J->count; i++) {
+        double w = oracle_rambo_point(J->n, J->sqrt_s, J->seed, i, mom);
+        int pass = 1;
+        for (int k = 1; k <= J->n; k++)
+            if (mom[8 + 4 * k] < J->omega_min) pass = 0;
+        double m = (double)point_msq(&P, mom, spec);
+        double v = pass ? w * m : 0;
+        double* c = J->partials + 3 * (i / J->chunk - J->c0);
+        c[0] += v;
+        c[1] += v * v;
+        c[2] += pass;
+    }
+    return NULL;
+}
+
+/* partials[3 * c + {0,1,2}] += (sum w|M|^2, sum (w|M|^2)^2, n_pass) for chunk c = index / chunk,
+   indices first .. first + count - 1; partials must hold ceil((first + count) / chunk) chunks.
+   Work is split over threads by whole chunks (each chunk summed in index order). */
+int oracle_mc_sum(int n_out_ph, double sqrt_s, double omega_min, uint64_t seed, uint64_t first, uint64_t count,
+                  int chunk, double* partials, int n_threads) {
+    if (n_out_ph < 1 || n_out_ph + 1 > MAX_PHOTONS || chunk < 1 || !(sqrt_s > 1)) return -1;
+    if (count == 0) return 0;
+    uint64_t c0 = first / chunk, c1 = (first + count + chunk - 1) / chunk;
+    uint64_t nch = c1 - c0;
+    if (n_threads < 1) n_threads = 1;
+    if ((uint64_t)n_threads > nch) n_threads = (int)nch;
+    if (n_threads > 256) n_threads = 256;
+    pthread_t th[256];
+    mc_job_t jobs[256];
+    for (int t = 0; t < n_threads; t++) {
+        uint64_t ca = c0 + nch * t / n_threads, cb = c0 + nch * (t + 1) / n_threads;
+        uint64_t lo = ca * chunk > first ? ca * chunk : first;
+        uint64_t hi = cb * chunk < first + count ? cb * chunk : first + count;
+        jobs[t] = (mc_job_t){n_out_ph, sqrt_s, omega_min, seed, lo, hi > lo ? hi - lo : 0, chunk,
+                             partials + 3 * ca, ca};
+        if (t > 0) pthread_create(&th[t], NULL, mc_worker, &jobs[t]);
+    }
+    mc_worker(&jobs[0]);
+    for (int t = 1; t < n_threads; t++) pthread_join(th[t], NULL);
+    return 0;
+}

@@ -43,6 +43,8 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     the default (chosen from measurements)."""
     wpb, mb = choose_launch(plan)
     mb4 = max(1, min(mb, 65536 // (152 * wpb * 32)))
+    if plan.N >= 5:   # r01 sweep: 4 partial accumulators win for n >= 4
+        return [(wpb, mb4, 4, 1), (wpb, mb, 2, 1), (wpb, mb, 2, 0)]
     return [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
 
 

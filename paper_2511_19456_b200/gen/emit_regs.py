@@ -206,9 +206,10 @@ void qedregs_config_N{N}(int variant, int* warps_per_block, int* points_per_warp
 
 def regs_variants(N: int) -> list[tuple[int, int, int]]:
     """Launch variants (warps per block, min resident blocks, L2 prefetch), QED_VARIANT selects."""
+    # variant 0 = best of the r01 sweep (profiles/sweep_r01.jsonl)
     if N == 3:
-        return [(2, 6, 1), (4, 1, 0), (4, 1, 1), (2, 6, 0), (2, 5, 1)]
-    return [(2, 8, 1), (4, 1, 0), (4, 1, 1), (2, 8, 0), (2, 6, 1)]
+        return [(4, 1, 1), (4, 1, 0), (2, 6, 1), (2, 6, 0), (2, 5, 1)]
+    return [(2, 6, 1), (4, 1, 0), (4, 1, 1), (2, 8, 0), (2, 8, 1)]
 
 
 def generate_regs(out_dir: str, Ns=(2, 3)) -> list[str]:

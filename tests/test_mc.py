@@ -1,0 +1,183 @@
+"""Monte-Carlo path: oracle pins (Philox KAT, RAMBO phase-space volumes, Klein-Nishina total
+cross-section), host-side sharding / reduction (gloo, 2 processes), and GPU parity of the
+fused qed_mc_sum kernel against the oracle."""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_19456_b200 import mc
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+ALPHA = 1 / 137.035999084
+
+
+def _kat():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")):
+        line = line.split("#")[0].strip()
+        if line:
+            v = [int(x, 16) for x in line.split()]
+            rows.append((v[0:4], v[4:6], v[6:10]))
+    return rows
+
+
+@pytest.mark.parametrize("ctr,key,expect", _kat())
+def test_philox_known_answers(ctr, key, expect):
+    assert oracle.philox4x32_10(ctr, key) == expect
+
+
+@pytest.mark.parametrize("n,sqrt_s", [(1, 5.0), (2, 1.5), (3, 5.0), (5, 20.0)])
+def test_rambo_points_on_shell_and_conserving(n, sqrt_s):
+    for idx in range(50):
+        m, w = oracle.rambo_point(n, sqrt_s, 9, idx)
+        tot_in = m[0] + m[1]
+        tot_out = m[2:].sum(0)
+        assert np.max(np.abs(tot_in - tot_out)) < 1e-12 * sqrt_s
+        assert np.allclose(tot_in, [sqrt_s, 0, 0, 0], atol=1e-13 * sqrt_s)
+        msq = m[:, 0] ** 2 - (m[:, 1:] ** 2).sum(1)
+        assert abs(msq[0] - 1) < 1e-12 * sqrt_s ** 2 and abs(msq[2] - 1) < 1e-12 * sqrt_s ** 2
+        assert np.all(np.abs(msq[[1] + list(range(3, n + 3))]) < 1e-12 * sqrt_s ** 2)
+        assert w > 0
+
+
+@pytest.mark.parametrize("sqrt_s", [1.5, 5.0, 100.0])
+def test_rambo_two_body_weight_is_the_phase_space_volume(sqrt_s):
+    """K = 2 (n = 1): every weight equals int dPhi_2 = |p*| / (4 pi sqrt s)."""
+    s = sqrt_s ** 2
+    pstar = (s - 1) / (2 * sqrt_s)
+    for idx in range(20):
+        _, w = oracle.rambo_point(1, sqrt_s, 3, idx)
+        assert abs(w / (pstar / (4 * math.pi * sqrt_s)) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("sqrt_s", [1.5, 5.0])
+def test_rambo_three_body_volume(sqrt_s):
+    """K = 3, masses (1, 0, 0): E[w] = Dalitz area / (128 pi^3 s), area = s^2/2 - s ln s - 1/2."""
+    s = sqrt_s ** 2
+    exact = (s * s / 2 - s * math.log(s) - 0.5) / (128 * math.pi ** 3 * s)
+    ws = np.array([oracle.rambo_point(2, sqrt_s, 5, i)[1] for i in range(40000)])
+    mean, err = ws.mean(), ws.std() / math.sqrt(len(ws))
+    assert abs(mean - exact) < 4 * err, (mean, exact, err)
+
+
+def test_klein_nishina_total_cross_section():
+    """n = 1, no cut: sigma_MC -> sigma_KN(x) = 2 pi r_e^2 {(1+x)/x^2 [2(1+x)/(1+2x) - ln(1+2x)/x]
+    + ln(1+2x)/(2x) - (1+3x)/(1+2x)^2}, r_e = alpha/m, x = (s - m^2)/(2 m^2)."""
+    sqrt_s = 2.0
+    N = 1 << 16
+    parts = oracle.mc_sum(1, sqrt_s, 0.0, 11, 0, N)
+    res = mc.cross_section(torch.from_numpy(parts), N, sqrt_s, 1)
+    s = sqrt_s ** 2
+    x = (s - 1) / 2
+    l = math.log(1 + 2 * x)
+    kn = 2 * math.pi * ALPHA ** 2 * ((1 + x) / x ** 2 * (2 * (1 + x) / (1 + 2 * x) - l / x) + l / (2 * x)
+                                     - (1 + 3 * x) / (1 + 2 * x) ** 2)
+    assert abs(res["sigma"] - kn) < 5 * res["error"], (res, kn)
+    assert res["error"] < 0.01 * kn
+    assert res["n_pass"] == N
+
+
+def test_chunked_sums_are_split_invariant():
+    """Chunk partials depend only on the global index range, not on how it is split."""
+    n, N = 2, 3 * mc.CHUNK + 100
+    whole = oracle.mc_sum(n, 5.0, 0.25, 4, 0, N, threads=3)
+    parts = np.zeros_like(whole)
+    for r in range(3):
+        first, count = mc.shard_range(N, r, 3)
+        local = oracle.mc_sum(n, 5.0, 0.25, 4, first, count, threads=1)
+        parts[: local.shape[0]] += local
+    assert np.array_equal(parts, whole)
+
+
+def test_shard_range_covers_and_aligns():
+    for N in (1, mc.CHUNK, 5 * mc.CHUNK + 7, 123456):
+        for world in (1, 2, 3, 8):
+            got = [mc.shard_range(N, r, world) for r in range(world)]
+            assert sum(c for _, c in got) == N
+            pos = 0
+            for first, count in got:
+                assert first == pos and (first % mc.CHUNK == 0 or count == 0)
+                pos += count
+
+
+# ---------------------------------------------------------------- gloo: 2 ranks on CPU
+
+def _gloo_worker(rank, world, port, N, out_path):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    partials = torch.zeros(3 * mc.n_chunks(N), dtype=torch.float64)
+    first, count = mc.shard_range(N, rank, world)
+    if count:
+        local = oracle.mc_sum(2, 5.0, 0.25, 21, first, count, threads=2)
+        partials[: local.size] += torch.from_numpy(local.reshape(-1))
+    mc.reduce_partials(partials)
+    res = mc.cross_section(partials, N, 5.0, 2)
+    if rank == 0:
+        torch.save({"partials": partials, "res": res}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_multi_rank_reduction_is_bitwise_identical(tmp_path):
+    import socket
+
+    import torch.multiprocessing as tmp
+    N = 2 * mc.CHUNK + 333
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = str(tmp_path / "r.pt")
+    tmp.spawn(_gloo_worker, args=(2, port, N, out), nprocs=2, join=True)
+    got = torch.load(out)
+    single = oracle.mc_sum(2, 5.0, 0.25, 21, 0, N, threads=4)
+    ref = mc.cross_section(torch.from_numpy(single.reshape(-1)), N, 5.0, 2)
+    assert torch.equal(got["partials"], torch.from_numpy(single.reshape(-1)))
+    assert got["res"]["sigma"] == ref["sigma"]
+
+
+# ---------------------------------------------------------------- GPU parity of qed_mc_sum
+
+MC_CASES = [(1, 20000, 0, 0.0), (2, 12000, 5000, 0.25), (3, 2500, 8000, 0.25), (4, 300, 8100, 0.25),
+            (5, 40, 16370, 0.25)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,count,first,omega_min", MC_CASES)
+def test_gpu_mc_sum_matches_oracle(n, count, first, omega_min):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_19456_b200 import qed
+    sqrt_s, seed = 5.0, 1234 + n
+    proc = qed.Process(n)
+    nch = mc.n_chunks(first + count)
+    partials = torch.zeros(3 * nch, dtype=torch.float64, device="cuda")
+    proc.mc_sum(partials, sqrt_s, omega_min, seed, first, count)
+    torch.cuda.synchronize()
+    got = partials.cpu().numpy().reshape(nch, 3)
+    ref = oracle.mc_sum(n, sqrt_s, omega_min, seed, first, count)
+    assert np.array_equal(got[:, 2], ref[:, 2])            # cut decisions identical
+    nz = ref[:, 0] > 0
+    assert np.all(np.abs(got[nz, :2] / ref[nz, :2] - 1) <= 1e-10)
+    assert np.all(got[~nz, :2] == 0)
+
+
+@pytest.mark.gpu
+def test_gpu_mc_cross_section_klein_nishina():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_19456_b200 import qed
+    sqrt_s, N = 2.0, 1 << 22
+    res = mc.mc_cross_section(qed.Process(1), sqrt_s, 0.0, 77, N)
+    s = sqrt_s ** 2
+    x = (s - 1) / 2
+    l = math.log(1 + 2 * x)
+    kn = 2 * math.pi * ALPHA ** 2 * ((1 + x) / x ** 2 * (2 * (1 + x) / (1 + 2 * x) - l / x) + l / (2 * x)
+                                     - (1 + 3 * x) / (1 + 2 * x) ** 2)
+    assert abs(res["sigma"] - kn) < 5 * res["error"]
+    assert res["error"] < 1e-3 * kn
