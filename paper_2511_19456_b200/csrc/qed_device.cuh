@@ -122,53 +122,28 @@ __device__ __forceinline__ spinor prop_row(const double* mk, const spinor& p) {
   return o;
 }
 
-// ---- task kinds (one trie node x one helicity state)
-// in-side V+S1 fused (interior levels and phi leaves): out = S(Q) epsslash parent
-__device__ __forceinline__ void task_vs_col(double* base, ushort4 t) {
-  spinor p = ld_spinor(base + t.x);
-  double2 e01 = *reinterpret_cast<const double2*>(base + t.y);
-  double e[3] = {e01.x, e01.y, base[t.y + 2]};
-  spinor v = eslash_col(e, p);
-  const double* mk = base + t.z;
-  double m5[5];
-  double2 m01 = *reinterpret_cast<const double2*>(mk);
-  double2 m23 = *reinterpret_cast<const double2*>(mk + 2);
-  m5[0] = m01.x; m5[1] = m01.y; m5[2] = m23.x; m5[3] = m23.y; m5[4] = mk[4];
-  st_spinor(base + t.w, prop_col(m5, v));
-}
-// out-side V+S1 fused (interior levels): out = (parent epsslash) S(Q)
-__device__ __forceinline__ void task_vs_row(double* base, ushort4 t) {
-  spinor p = ld_spinor(base + t.x);
-  double2 e01 = *reinterpret_cast<const double2*>(base + t.y);
-  double e[3] = {e01.x, e01.y, base[t.y + 2]};
-  spinor v = eslash_row(e, p);
-  const double* mk = base + t.z;
-  double m5[5];
-  double2 m01 = *reinterpret_cast<const double2*>(mk);
-  double2 m23 = *reinterpret_cast<const double2*>(mk + 2);
-  m5[0] = m01.x; m5[1] = m01.y; m5[2] = m23.x; m5[3] = m23.y; m5[4] = mk[4];
-  st_spinor(base + t.w, prop_row(m5, v));
-}
-// out-side leaf: out = parent epsslash
-__device__ __forceinline__ void task_v_row(double* base, ushort4 t) {
-  spinor p = ld_spinor(base + t.x);
-  double2 e01 = *reinterpret_cast<const double2*>(base + t.y);
-  double e[3] = {e01.x, e01.y, base[t.y + 2]};
-  st_spinor(base + t.w, eslash_row(e, p));
-}
-
 // ---- external states (U): written to shared memory
 // eps(k, 1) = (cos t cos f, cos t sin f, -sin t), eps(k, 2) = (-sin f, cos f, 0),
 // t = atan2(k_perp, k_z), f = atan2(k_y, k_x) (f := 0 for k_perp = 0)      [SURVEY.md §8(c) item 4]
-__device__ __forceinline__ void external_eps(const double* k, double* out /* [2][4] */) {
-  double kperp = sqrt(k[1] * k[1] + k[2] * k[2]);
-  double kn = sqrt(kperp * kperp + k[3] * k[3]);
-  double ct = k[3] / kn, st = kperp / kn;
-  double cf = 1.0, sf = 0.0;
-  if (kperp > 0.0) {
-    cf = k[1] / kperp;
-    sf = k[2] / kperp;
+// cos t = k_z / |k|, sin t = k_perp / |k|, cos f = k_x / k_perp, sin f = k_y / k_perp, evaluated with two
+// reciprocal square roots (MUFU + Newton, <= 1 ulp) instead of two sqrt and four IEEE divisions.
+__device__ __forceinline__ void eps_consts(const double* k, double& ct, double& st, double& cf, double& sf) {
+  const double kp2 = k[1] * k[1] + k[2] * k[2];
+  const double rkn = rsqrt(fma(k[3], k[3], kp2));
+  double rkp = 0.0;
+  cf = 1.0;
+  sf = 0.0;
+  if (kp2 > 0.0) {
+    rkp = rsqrt(kp2);
+    cf = k[1] * rkp;
+    sf = k[2] * rkp;
   }
+  ct = k[3] * rkn;
+  st = (kp2 * rkp) * rkn;
+}
+__device__ __forceinline__ void external_eps(const double* k, double* out /* [2][4] */) {
+  double ct, st, cf, sf;
+  eps_consts(k, ct, st, cf, sf);
   reinterpret_cast<double2*>(out)[0] = make_double2(ct * cf, ct * sf);
   reinterpret_cast<double2*>(out)[1] = make_double2(-st, 0.0);
   reinterpret_cast<double2*>(out)[2] = make_double2(-sf, cf);
@@ -176,7 +151,7 @@ __device__ __forceinline__ void external_eps(const double* k, double* out /* [2]
 }
 // u(p, s) = (n chi_s, sigma.p chi_s / n), n = sqrt(E + m)      [SURVEY.md §8(c) item 3]
 __device__ __forceinline__ void external_u(const double* p, double* out /* [2][8] */) {
-  double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  const double r = rsqrt(p[0] + 1.0), n = (p[0] + 1.0) * r;
   double* o = out;
   st2(o + 0, {n, 0}); st2(o + 2, {0, 0}); st2(o + 4, {p[3] * r, 0}); st2(o + 6, {p[1] * r, p[2] * r});
   o += 8;
@@ -184,7 +159,7 @@ __device__ __forceinline__ void external_u(const double* p, double* out /* [2][8
 }
 // ubar(p', s') = u(p', s')^dagger gamma^0
 __device__ __forceinline__ void external_ubar(const double* p, double* out /* [2][8] */) {
-  double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  const double r = rsqrt(p[0] + 1.0), n = (p[0] + 1.0) * r;
   double* o = out;
   st2(o + 0, {n, 0}); st2(o + 2, {0, 0}); st2(o + 4, {-p[3] * r, 0}); st2(o + 6, {-p[1] * r, p[2] * r});
   o += 8;

@@ -113,7 +113,7 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
       external_eps(base + T::MOM + 4 * ((a.photon_particle >> (4 * t)) & 15), base + T::EPS + 8 * t);
     } else if (t == N) {
       const double* p = base + T::MOM;
-      const double nn = sqrt(p[0] + 1.0), r = 1.0 / nn;
+      const double r = rsqrt(p[0] + 1.0), nn = (p[0] + 1.0) * r;
       spinor u0, u1;   // u(p, s) = (n chi_s, sigma.p chi_s / n)
       u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {p[3] * r, 0}; u0.v[3] = {p[1] * r, p[2] * r};
       u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {p[1] * r, -p[2] * r}; u1.v[3] = {-p[3] * r, 0};
@@ -121,7 +121,7 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
       st_aos(base, T::U + 8, u1);
     } else if (t == N + 1) {
       const double* p = base + T::MOM + 4 * a.e_out_particle;
-      const double nn = sqrt(p[0] + 1.0), r = 1.0 / nn;
+      const double r = rsqrt(p[0] + 1.0), nn = (p[0] + 1.0) * r;
       spinor u0, u1;   // ubar(p', s') = u^dagger gamma^0
       u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {-p[3] * r, 0}; u0.v[3] = {-p[1] * r, p[2] * r};
       u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {-p[1] * r, -p[2] * r}; u1.v[3] = {p[3] * r, 0};

@@ -13,6 +13,9 @@
 namespace qed {
 
 
+// momentum element: global (read-only path) or the cp.async staging buffer in shared memory
+__device__ __forceinline__ double ld_mom(const double* p) { return *p; }
+
 // eps(k, 1), eps(k, 2) as in external_eps, into registers
 __device__ __forceinline__ void eps_regs(const double* k, double (&e)[2][3]) {
   const double kperp = sqrt(k[1] * k[1] + k[2] * k[2]);
@@ -29,7 +32,7 @@ __device__ __forceinline__ void eps_regs(const double* k, double (&e)[2][3]) {
 
 // u(p, s) = (n chi_s, sigma.p chi_s / n), n = sqrt(E + m)
 __device__ __forceinline__ spinor u_spinor(const double* p, int s) {
-  const double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  const double r = rsqrt(p[0] + 1.0), n = (p[0] + 1.0) * r;
   spinor u;
   if (s == 0) {
     u.v[0] = {n, 0}; u.v[1] = {0, 0}; u.v[2] = {p[3] * r, 0}; u.v[3] = {p[1] * r, p[2] * r};
@@ -41,7 +44,7 @@ __device__ __forceinline__ spinor u_spinor(const double* p, int s) {
 
 // ubar(p', s') = u(p', s')^dagger gamma^0
 __device__ __forceinline__ spinor ubar_spinor(const double* p, int s) {
-  const double n = sqrt(p[0] + 1.0), r = 1.0 / n;
+  const double r = rsqrt(p[0] + 1.0), n = (p[0] + 1.0) * r;
   spinor u;
   if (s == 0) {
     u.v[0] = {n, 0}; u.v[1] = {0, 0}; u.v[2] = {-p[3] * r, 0}; u.v[3] = {-p[1] * r, p[2] * r};
@@ -101,28 +104,90 @@ __device__ __forceinline__ void cdot_acc(const spinor& a, const spinor& b, doubl
   }
 }
 
-// V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, PF L2 prefetch)
+// V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, PF L2 prefetch).
+// T: generated body; T::TPP threads per point (2: thread = (point, s'); 4: (point, s', lam_0)),
+// T::NACC amplitudes per thread, T::config_of(idx, sub) = internal configuration index.
+// cp.async staging of one warp's batch of momenta: rows 4(N+2) x PPW points, 8-byte copies
+template <int ROWS, int PPW>
+__device__ __forceinline__ void stage_batch(double* dst, const double* __restrict__ mom, long long n, long long p0, int lane) {
+#pragma unroll
+  for (int e = lane; e < ROWS * PPW; e += 32) {
+    const int r = e / PPW, q = e % PPW;
+    long long pt = p0 + q;
+    pt = pt < n ? pt : n - 1;
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(mom + (long long)r * n + pt) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// 8 joins of one out-side block, DFMAs interleaved across the pairs: pairs (l0, ph[k]) -> acc[ix[k]],
+// (l1, ph[k]) -> acc[ix[4 + k]]
+template <int NA>
+__device__ __forceinline__ void cdot8_acc(const spinor& l0, const spinor& l1, const spinor (&ph)[4], const int (&ix)[8],
+                                          double (&acc)[NA]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const spinor& L = q < 4 ? l0 : l1;
+      const c2 b = ph[q & 3].v[c];
+      acc[2 * ix[q]] = fma(-L.v[c].i, b.i, acc[2 * ix[q]]);
+      acc[2 * ix[q] + 1] = fma(L.v[c].i, b.r, acc[2 * ix[q] + 1]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const spinor& L = q < 4 ? l0 : l1;
+      const c2 b = ph[q & 3].v[c];
+      acc[2 * ix[q]] = fma(L.v[c].r, b.r, acc[2 * ix[q]]);
+      acc[2 * ix[q] + 1] = fma(L.v[c].r, b.i, acc[2 * ix[q] + 1]);
+    }
+  }
+}
+
 template <class T, class V, bool PER_CONFIG>
 __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int N = T::N;
-  constexpr int NACC = 1 << (N + 1);       // configurations (s, lam_1..lam_N) per thread
+  constexpr int TPP = T::TPP;
+  constexpr int PPW = 32 / TPP;            // points per warp
+  constexpr int NACC = T::NACC;
+  constexpr int ROWS = 4 * (N + 2);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int sp = lane & 1;
-  double* sl = smem + (warp * 16 + (lane >> 1)) * T::STRIDE;
+  const int sub = lane % TPP;
+  double* sl = smem + (warp * PPW + lane / TPP) * T::STRIDE;
+  // PF == 2: double-buffered cp.async staging of the momenta (after the point slots)
+  double* stage = smem + V::WPB * PPW * T::STRIDE + warp * 2 * ROWS * PPW;
   const long long n = a.n_points;
   const long long warps_total = (long long)gridDim.x * V::WPB;
+  const long long first = ((long long)blockIdx.x * V::WPB + warp) * PPW;
+  if (V::PF == 2 && first < n) stage_batch<ROWS, PPW>(stage, a.mom, n, first, lane);
+  int buf = 0;
 #pragma unroll 1
-  for (long long p0 = ((long long)blockIdx.x * V::WPB + warp) * 16; p0 < n; p0 += warps_total * 16) {
-    const long long pt = p0 + (lane >> 1);
+  for (long long p0 = first; p0 < n; p0 += warps_total * PPW) {
+    const long long pt = p0 + lane / TPP;
     const bool valid = pt < n;
     const long long ptc = valid ? pt : n - 1;
-    {
-      // L2 prefetch of this warp's next batch of momenta (one 128-byte row per lane), so the
-      // next iteration's loads do not wait on HBM latency.
-      const long long nx = p0 + warps_total * 16;
-      if (V::PF && lane < 4 * (N + 2) && nx < n) {
+    const double* msrc = a.mom;
+    long long mstride = n, mpt = ptc;
+    if (V::PF == 2) {
+      const long long nx = p0 + warps_total * PPW;
+      if (nx < n) {
+        stage_batch<ROWS, PPW>(stage + (buf ^ 1) * ROWS * PPW, a.mom, n, nx, lane);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      msrc = stage + buf * ROWS * PPW;
+      mstride = PPW;
+      mpt = lane / TPP;
+      buf ^= 1;
+    } else if (V::PF == 1) {
+      // L2 prefetch of this warp's next batch of momenta (one row per lane)
+      const long long nx = p0 + warps_total * PPW;
+      if (lane < ROWS && nx < n) {
         const double* r = a.mom + (long long)lane * n + nx;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
       }
@@ -130,12 +195,12 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
     double acc[2 * NACC];
 #pragma unroll
     for (int i = 0; i < 2 * NACC; ++i) acc[i] = 0.0;
-    T::body(a.mom, n, ptc, sp, sl, a, acc);
+    T::body(msrc, mstride, mpt, sub, sl, a, acc);
     if (PER_CONFIG) {
       if (valid) {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {
-          const unsigned h = idx | (sp << (N + 1));
+          const unsigned h = T::config_of(idx, sub);
           unsigned hx = 0;
 #pragma unroll
           for (int b = 0; b < N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
@@ -150,15 +215,16 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
       } else {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {
-          const unsigned h = idx | (sp << (N + 1));
+          const unsigned h = T::config_of(idx, sub);
           const double t = fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
           sum += ((h & a.fixed_mask) == a.fixed_val) ? t : 0.0;
         }
       }
-      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-      if (valid && sp == 0) a.out[pt] = a.norm * sum;
+#pragma unroll
+      for (int o = 1; o < TPP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (valid && sub == 0) a.out[pt] = a.norm * sum;
     }
-    __syncwarp();  // phi slot reused by the next point
+    __syncwarp();  // the slot is reused by the next point
   }
 }
 

@@ -74,28 +74,27 @@ def emit_regs_body(N: int) -> str:
     w("  const int e_out = a.e_out_particle;")
     w("  double pe[4], pp[4];")
     w("  for (int mu = 0; mu < 4; ++mu) {")
-    w("    pe[mu] = __ldg(mom + (long long)mu * n + pt);")
-    w("    pp[mu] = __ldg(mom + (long long)(4 * e_out + mu) * n + pt);")
+    w("    pe[mu] = qed::ld_mom(mom + (long long)mu * n + pt);")
+    w("    pp[mu] = qed::ld_mom(mom + (long long)(4 * e_out + mu) * n + pt);")
     w("  }")
-    w("  if (sp == 0) {")
-    w("    // polarisation vectors of every photon -> slot EPS")
-    w(f"    for (int i = 0; i < {N}; ++i) {{")
-    w("      const int pj = (a.photon_particle >> (4 * i)) & 15;")
-    w("      double k[4];")
-    w("      for (int mu = 0; mu < 4; ++mu) k[mu] = __ldg(mom + (long long)(4 * pj + mu) * n + pt);")
-    w(f"      qed::external_eps(k, sl + {lay['EPS']} + 8 * i);")
-    w("    }")
-    w("  } else {")
-    w("    // propagator constants: in-side leaves S(Q_{a}), out-side interiors S(Q_{all \\ b})")
+    w("  // external polarisations and propagator constants, split evenly over the two threads of the")
+    w("  // point without divergence: thread s' takes photons i = s', s'+2, ... and subsets k = s', s'+2, ...")
+    w(f"  for (int i = sp; i < {N}; i += 2) {{")
+    w("    const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("    double k[4];")
+    w("    for (int mu = 0; mu < 4; ++mu) k[mu] = qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w(f"    qed::external_eps(k, sl + {lay['EPS']} + 8 * i);")
+    w("  }")
+    w("  {")
     w(f"    double q[{N}][4];")
     w(f"    for (int i = 0; i < {N}; ++i) {{")
     w("      const int pj = (a.photon_particle >> (4 * i)) & 15;")
     w("      const double sg = i < a.n_in_ph ? 1.0 : -1.0;")
-    w("      for (int mu = 0; mu < 4; ++mu) q[i][mu] = sg * __ldg(mom + (long long)(4 * pj + mu) * n + pt);")
+    w("      for (int mu = 0; mu < 4; ++mu) q[i][mu] = sg * qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
     w("    }")
     masks = [1 << i for i in range(N)] + ([full & ~(1 << b) for b in range(N)] if N == 3 else [])
-    for k, msk in enumerate(masks):
-        w(f"    qed::mask_store(pe, q, {msk}, sl + {lay['MASK']} + {6 * k});")
+    w(f"    for (int k = sp; k < {len(masks)}; k += 2)   // subsets: k < N -> {{k}}, k >= N -> all \\ {{k - N}}")
+    w(f"      qed::mask_store(pe, q, k < {N} ? (1 << k) : ({full} & ~(1 << (k - {N}))), sl + {lay['MASK']} + 6 * k);")
     w("  }")
     w("  const qed::spinor u = qed::u_spinor(pe, sp);      // u(p, s = s'): this thread's half of phi")
     w("  const qed::spinor ub = qed::ubar_spinor(pp, sp);  // ubar(p', s')")
@@ -150,41 +149,194 @@ def emit_regs_body(N: int) -> str:
     return "\n".join(L) + "\n"
 
 
+def emit_regs_body4(N: int) -> str:
+    """N = 3 body with four threads per point: thread = (point, s', lam_0).  Photon 0's polarisation
+    is fixed per thread, so out-side nodes that do not involve photon 0 are computed by both lam_0
+    threads (+14 % executed flops) in exchange for half the accumulators (more resident warps)."""
+    assert N == 3
+    lay = slot_layout(N)
+    full = (1 << N) - 1
+    L = []
+    w = L.append
+    w(f"// ---- generated straight-line body, N = {N} (thread = point x s' x lam_0), j = 1")
+    w("template <class ARGS>")
+    w(f"__device__ __forceinline__ void regs_body4_N{N}(const double* __restrict__ mom, long long n, long long pt, int sub,")
+    w("                                               double* __restrict__ sl, const ARGS& a, double (&acc)[16]) {")
+    w("  const int sp = sub & 1, l0 = sub >> 1;")
+    w("  const int e_out = a.e_out_particle;")
+    w("  double pe[4], pp[4];")
+    w("  for (int mu = 0; mu < 4; ++mu) {")
+    w("    pe[mu] = qed::ld_mom(mom + (long long)mu * n + pt);")
+    w("    pp[mu] = qed::ld_mom(mom + (long long)(4 * e_out + mu) * n + pt);")
+    w("  }")
+    w("  if (sub == 0) {")
+    w(f"    for (int i = 0; i < {N}; ++i) {{")
+    w("      const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("      double k[4];")
+    w("      for (int mu = 0; mu < 4; ++mu) k[mu] = qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w(f"      qed::external_eps(k, sl + {lay['EPS']} + 8 * i);")
+    w("    }")
+    w("  } else if (sub == 1 || sub == 2) {")
+    w(f"    double q[{N}][4];")
+    w(f"    for (int i = 0; i < {N}; ++i) {{")
+    w("      const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("      const double sg = i < a.n_in_ph ? 1.0 : -1.0;")
+    w("      for (int mu = 0; mu < 4; ++mu) q[i][mu] = sg * qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w("    }")
+    masks = [1 << i for i in range(N)] + [full & ~(1 << b) for b in range(N)]
+    w("    if (sub == 1) {")
+    for k, msk in enumerate(masks[:3]):
+        w(f"      qed::mask_store(pe, q, {msk}, sl + {lay['MASK']} + {6 * k});")
+    w("    } else {")
+    for k, msk in enumerate(masks[3:]):
+        w(f"      qed::mask_store(pe, q, {msk}, sl + {lay['MASK']} + {6 * (k + 3)});")
+    w("    }")
+    w("  }")
+    w("  __syncwarp();")
+    w("  // in-side leaves phi_a[s][lam]: 12 spinors, 3 per thread (entry e = 4 k + sub)")
+    w("  #pragma unroll")
+    w("  for (int k = 0; k < 3; ++k) {")
+    w("    const int e = 4 * k + sub, ai = e >> 2, s = (e >> 1) & 1, lam = e & 1;")
+    w("    const qed::spinor u = qed::u_spinor(pe, s);")
+    w(f"    qed::st_spinor(sl + e * 8, qed::prop_col(sl + {lay['MASK']} + 6 * ai, qed::eslash_col(sl + {lay['EPS']} + 8 * ai + 4 * lam, u)));")
+    w("  }")
+    w("  const qed::spinor ub = qed::ubar_spinor(pp, sp);  // ubar(p', s')")
+    w("  __syncwarp();")
+    for b in range(N):
+        lbs = ["l0"] if b == 0 else ["0", "1"]
+        for lb in lbs:
+            lb_bit = "" if b == 0 else f" | ({lb} << {b})"   # acc idx: s | lam1 << 1 | lam2 << 2
+            w(f"  {{  // tau_1 = photon {b}, lam_{b} = {lb}")
+            w("    __syncwarp();")
+            w(f"    double eb[3], mb[5]; qed::ld_stream_eps(sl + {lay['EPS']} + 8 * {b} + 4 * ({lb}), eb); "
+              f"qed::ld_stream_mask(sl + {lay['MASK'] + 6 * (N + b)}, mb);")
+            w("    const qed::spinor I = qed::prop_row(mb, qed::eslash_row(eb, ub));")
+            for c in range(N):
+                if c == b:
+                    continue
+                a_ = 3 - b - c
+                lcs = ["l0"] if c == 0 else ["0", "1"]
+                w(f"    {{  // tau_2 = photon {c}, remaining photon {a_}")
+                w("      __syncwarp();")
+                for li, lc in enumerate(lcs):
+                    w(f"      double ec{li}[3]; qed::ld_stream_eps(sl + {lay['EPS']} + 8 * {c} + 4 * ({lc}), ec{li});")
+                    w(f"      const qed::spinor lf{li} = qed::eslash_row(ec{li}, I);")
+                # phi_a[s][lam_a]: lam_a = l0 if a == 0 else both
+                las = ["l0"] if a_ == 0 else ["0", "1"]
+                w("      #pragma unroll")
+                w("      for (int s = 0; s < 2; ++s) {")
+                for la in las:
+                    w(f"        {{ const qed::spinor ph = qed::ld_spinor_stream(sl + (({a_} * 2 + s) * 2 + ({la})) * 8);")
+                    for li, lc in enumerate(lcs):
+                        bits = []
+                        for (ph_, lam) in ((b, lb), (c, lc), (a_, la)):
+                            if ph_ != 0:
+                                bits.append(f"(({lam}) << {ph_})")
+                        idx = "s | " + " | ".join(bits) if bits else "s"
+                        w(f"          {{ const int idx = {idx}; qed::cdot_acc(lf{li}, ph, acc[2 * idx], acc[2 * idx + 1]); }}")
+                    w("        }")
+                w("      }")
+                w("    }")
+            w("  }")
+    w("  __syncwarp();")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
+def emit_regs_body_interleaved(N: int) -> str:
+    """Same DAG and thread mapping as emit_regs_body(3), but each (b, lam_b, c) block loads its four
+    phi spinors first and issues the 8 joins' DFMAs interleaved (8 independent chains in a row)."""
+    assert N == 3
+    src = emit_regs_body(N)
+    src = src.replace(f"regs_body_N{N}(", f"regs_bodyi_N{N}(")
+    lines = src.split("\n")
+    out = []
+    i = 0
+    while i < len(lines):
+        ln = lines[i]
+        if ln.strip() == "#pragma unroll" and i + 1 < len(lines) and "for (int k = 0; k < 4; ++k) {" in lines[i + 1] \
+                and "ld_spinor_stream" in lines[i + 2] and "i0 =" in lines[i + 3]:
+            # lines: pragma, for, ph load, i0, cdot l0, cdot l1, close
+            load = lines[i + 2].strip()
+            i0 = lines[i + 3].strip()
+            bit = lines[i + 5].split("(i0 | ")[1].split(")")[0]
+            ind = ln[: len(ln) - len(ln.lstrip())]
+            base_expr = load.split("ld_spinor_stream(")[1].rsplit(");", 1)[0]
+            i0_expr = i0.split("=", 1)[1].strip().rstrip(";")
+            out.append(f"{ind}qed::spinor ph[4];")
+            out.append(f"{ind}#pragma unroll")
+            out.append(f"{ind}for (int k = 0; k < 4; ++k) ph[k] = qed::ld_spinor_stream({base_expr});")
+            out.append(f"{ind}int ix[8];")
+            out.append(f"{ind}#pragma unroll")
+            out.append(f"{ind}for (int k = 0; k < 4; ++k) {{ ix[k] = {i0_expr}; ix[4 + k] = ix[k] | {bit}; }}")
+            out.append(f"{ind}qed::cdot8_acc(l0, l1, ph, ix, acc);")
+            i += 7
+            continue
+        out.append(ln)
+        i += 1
+    return "\n".join(out)
+
+
 def emit_regs_source(N: int) -> str:
     fl = _flops(N)
     total = sum(fl.values())
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in fl.items())
     vs = regs_variants(N)
     ns = f"qedregs_N{N}"
-    variant_structs = "namespace " + ns + " {\n" + "".join(
+    lay = slot_layout(N)
+    variant_structs = "".join(
         f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, PF = {p}; }};\n"
-        for i, (w, m, p) in enumerate(vs)) + "}\n"
+        for i, (d, w, m, p) in enumerate(vs))
     kernel_cases = "\n".join(
-        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::T, {ns}::V{i}, true>\n"
-        f"                                      : (const void*)qed::qed_regs_kernel<{ns}::T, {ns}::V{i}, false>;"
-        for i in range(len(vs)))
+        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, true>\n"
+        f"                                      : (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, false>;"
+        for i, (d, w, m, p) in enumerate(vs))
+    tpp = "{" + ", ".join("4" if d == "T4" else "2" for d, *_ in vs) + "}"
+    body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) if N == 3 else ""
+    t4 = f"""
+// four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
+struct T4 {{
+  static constexpr int N = {N}, TPP = 4, NACC = 8, STRIDE = {lay['STRIDE']};
+  template <class ARGS2>
+  static __device__ __forceinline__ void body(const double* mom, long long n, long long pt, int sub, double* sl,
+                                              const ARGS2& a, double (&acc)[16]) {{
+    regs_body4_N{N}(mom, n, pt, sub, sl, a, acc);
+  }}
+  static __device__ __forceinline__ unsigned config_of(int idx, int sub) {{
+    return (idx & 1) | ((unsigned)(sub >> 1) << 1) | ((unsigned)(idx >> 1) << 2) | ((unsigned)(sub & 1) << (N + 1));
+  }}
+}};
+// two threads per point, joins issued interleaved across the 8 (leaf, phi) pairs of a block
+struct TI : T {{
+  template <class ARGS2>
+  static __device__ __forceinline__ void body(const double* mom, long long n, long long pt, int sub, double* sl,
+                                              const ARGS2& a, double (&acc)[{2 << (N + 1)}]) {{
+    regs_bodyi_N{N}(mom, n, pt, sub, sl, a, acc);
+  }}
+}};""" if N == 3 else ""
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_regs.py -- do not edit.
-// Register-resident kernel for N = {N} photons (n = {N - 1}); thread = (point, s').
+// Register-resident kernel for N = {N} photons (n = {N - 1}); thread = (point, s') [T] or (point, s', lam_0) [T4].
 // Algorithmic FP64 flops per point:
 {flops_comment}
 //   {'total':22s} {total:>10d}
 #include "../qed_eval_regs.cuh"
 
-namespace qedregs_N{N} {{
+namespace {ns} {{
 {emit_regs_body(N)}
+{body4}
+// two threads per point: (point, s'); accumulators s | lam_i << (1 + i)
 struct T {{
-  static constexpr int N = {N};
+  static constexpr int N = {N}, TPP = 2, NACC = {1 << (N + 1)}, STRIDE = {lay['STRIDE']};
   static constexpr long long FLOPS_PER_POINT = {total}LL;
-  static constexpr int STRIDE = {slot_layout(N)['STRIDE']};
   template <class ARGS2>
-  static __device__ __forceinline__ void body(const double* mom, long long n, long long pt, int sp, double* sl,
+  static __device__ __forceinline__ void body(const double* mom, long long n, long long pt, int sub, double* sl,
                                               const ARGS2& a, double (&acc)[{2 << (N + 1)}]) {{
-    regs_body_N{N}(mom, n, pt, sp, sl, a, acc);
+    regs_body_N{N}(mom, n, pt, sub, sl, a, acc);
   }}
-}};
-}}  // namespace qedregs_N{N}
+  static __device__ __forceinline__ unsigned config_of(int idx, int sub) {{ return idx | ((unsigned)sub << (N + 1)); }}
+}};{t4}
+{variant_structs}}}  // namespace {ns}
 
-{variant_structs}
 extern "C" {{
 int qedregs_num_variants_N{N}(void) {{ return {len(vs)}; }}
 const void* qedregs_kernel_N{N}(int per_config, int variant) {{
@@ -194,22 +346,26 @@ const void* qedregs_kernel_N{N}(int per_config, int variant) {{
 }}
 void qedregs_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, long long* smem_per_block,
                          long long* flops_per_point) {{
-  static const int wpb[{len(vs)}] = {{{", ".join(str(v[0]) for v in vs)}}};
+  static const int wpb[{len(vs)}] = {{{", ".join(str(v[1]) for v in vs)}}};
+  static const int tpp[{len(vs)}] = {tpp};
   *warps_per_block = wpb[variant];
-  *points_per_warp = 16;
-  *smem_per_block = (long long)wpb[variant] * 16 * qedregs_N{N}::T::STRIDE * 8;
-  *flops_per_point = qedregs_N{N}::T::FLOPS_PER_POINT;
+  *points_per_warp = 32 / tpp[variant];
+  static const int pf[{len(vs)}] = {{{", ".join(str(v[3]) for v in vs)}}};
+  *smem_per_block = (long long)wpb[variant] * (32 / tpp[variant]) * {ns}::T::STRIDE * 8 +
+                    (pf[variant] == 2 ? (long long)wpb[variant] * 2 * {4 * (N + 2)} * (32 / tpp[variant]) * 8 : 0);
+  *flops_per_point = {ns}::T::FLOPS_PER_POINT;
 }}
 }}
 """
 
 
-def regs_variants(N: int) -> list[tuple[int, int, int]]:
-    """Launch variants (warps per block, min resident blocks, L2 prefetch), QED_VARIANT selects."""
-    # variant 0 = best of the r01 sweep (profiles/sweep_r01.jsonl)
+def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
+    """Launch variants (body, warps per block, min resident blocks, L2 prefetch); QED_VARIANT selects.
+    Variant 0 = best of the latest sweep (profiles/sweep_*.jsonl)."""
     if N == 3:
-        return [(4, 1, 1), (4, 1, 0), (2, 6, 1), (2, 6, 0), (2, 5, 1)]
-    return [(2, 6, 1), (4, 1, 0), (4, 1, 1), (2, 8, 0), (2, 8, 1)]
+        return [("T", 4, 1, 2), ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2),
+                ("TI", 4, 1, 2), ("TI", 4, 1, 1)]
+    return [("T", 2, 6, 2), ("T", 4, 1, 0), ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
 
 
 def generate_regs(out_dir: str, Ns=(2, 3)) -> list[str]:
