@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-per-n", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning sweeps)")
+    ap.add_argument("--algorithm", default="cdag", choices=["cdag", "bg"],
+                    help="cdag: the paper's node-reduced diagram DAG (headline); bg: Berends-Giele rewrite")
     return ap.parse_args()
 
 
@@ -236,6 +238,31 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- our arm
+def sweep_per_n(args, world, stream, dev, algorithm: str) -> dict:
+    """Every process size n = 1..5 at its own batch size, same timing protocol, 5 steps."""
+    import torch
+
+    import synthetic
+    from paper_2511_19456_b200 import qed
+    out = {}
+    for m in range(1, 6):
+        Pm = PER_N_POINTS[m] * (4 if algorithm == "bg" and m >= 4 else 1)
+        pm = qed.Process(m, algorithm=algorithm)
+        mm = synthetic.rambo_cm(m, Pm, sqrt_s=args.sqrt_s, seed=7 + m, device=dev)
+        sm = synthetic.to_soa(mm)
+        del mm
+        om = torch.empty(Pm, dtype=torch.float64, device=dev)
+        tm, perm = time_device(lambda: pm.eval_msq(sm, om, Pm, stream=stream), 5, 3, world, stream)
+        fm = pm.info()["flops_per_point"]
+        ks = statistics.mean(perm) / 1e3
+        out[str(m)] = {"points_per_gpu": Pm, "value": world * Pm * 5 / tm, "unit": UNIT,
+                       "ms_per_step": 1e3 * tm / 5, "flops_per_point": fm,
+                       "achieved_tflops": round(fm * Pm / ks / 1e12, 3),
+                       "frac_fp64_peak": round(fm * Pm / ks / 1e12 / FP64_PEAK_TFLOPS, 4)}
+        del sm, om, pm
+    return out
+
+
 def run_e2e(args, world, proc, soa, P) -> dict:
     """Same metric through the public host-buffer API (qed_eval_msq_host): every step copies the
     step's momenta H2D from pinned memory, evaluates, and copies |M|^2 back D2H."""
@@ -261,7 +288,7 @@ def run_b200(args, world, rank, local):
     n, P = args.n, args.points
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    proc = qed.Process(n)
+    proc = qed.Process(n, algorithm=args.algorithm)
     info = proc.info()
     # each rank owns its own shard of points (weak scaling): seed depends on the rank
     mom = synthetic.rambo_cm(n, P, sqrt_s=args.sqrt_s, seed=args.seed * 1000 + rank, device=dev)
@@ -302,24 +329,10 @@ def run_b200(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, world, proc, soa, P)
-    per_n = None
+    per_n = per_n_bg = None
     if not args.no_per_n:
-        per_n = {}
-        for m in range(1, 6):
-            Pm = PER_N_POINTS[m]
-            pm = qed.Process(m)
-            mm = synthetic.rambo_cm(m, Pm, sqrt_s=args.sqrt_s, seed=7 + m, device=dev)
-            sm = synthetic.to_soa(mm)
-            del mm
-            om = torch.empty(Pm, dtype=torch.float64, device=dev)
-            tm, perm = time_device(lambda: pm.eval_msq(sm, om, Pm, stream=stream), 5, 3, world, stream)
-            fm = pm.info()["flops_per_point"]
-            ks = statistics.mean(perm) / 1e3
-            per_n[str(m)] = {"points_per_gpu": Pm, "value": world * Pm * 5 / tm, "unit": UNIT,
-                             "ms_per_step": 1e3 * tm / 5, "flops_per_point": fm,
-                             "achieved_tflops": round(fm * Pm / ks / 1e12, 3),
-                             "frac_fp64_peak": round(fm * Pm / ks / 1e12 / FP64_PEAK_TFLOPS, 4)}
-            del sm, om, pm
+        per_n = sweep_per_n(args, world, stream, dev, "cdag")
+        per_n_bg = sweep_per_n(args, world, stream, dev, "bg")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -332,7 +345,8 @@ def run_b200(args, world, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[1]: e-gamma->e-+{n}gamma ({math.factorial(n + 1)} diagrams), "
+            "config": {"algorithm": args.algorithm,
+                       "workload": f"BASELINE configs[1]: e-gamma->e-+{n}gamma ({math.factorial(n + 1)} diagrams), "
                                    f"{P} RAMBO points/GPU, sqrt(s)={args.sqrt_s}, pol-summed/averaged |M|^2",
                        "n": n, "global_batch": world * P, "points_per_gpu": P,
                        "parallelism": f"points sharded over {world} GPU(s), no collective",
@@ -341,6 +355,7 @@ def run_b200(args, world, rank, local):
                                                             "grid_blocks")}, variant=os.environ.get("QED_VARIANT", "0"))},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "fp64_dfma_microbench": peak, "per_n": per_n,
+            "per_n_berends_giele": per_n_bg,
         }
         print(json.dumps(line), flush=True)
 

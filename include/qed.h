@@ -70,6 +70,21 @@ typedef struct qed_process qed_process; /* opaque, owned by libqed */
 qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
                               qed_process** proc);
 
+/* Algorithm selection (extension).  QED_ALGO_CDAG (default) evaluates the paper's node-reduced
+   diagram DAG: every one of the (n+1)! diagrams is joined separately (App. C).
+   QED_ALGO_BERENDS_GIELE applies the distributive term rewriting the paper names as the route to
+   exponential scaling: the sum over the
+   orderings of each photon subset is taken inside the propagators (Berends-Giele currents), one join
+   per subset.  Same |M|^2 (same oracle), fewer flops: 7.8 k vs 10.7 k (n = 2), 310 k vs 6.2 M (n = 5).
+   variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable. */
+typedef enum { QED_ALGO_CDAG = 0, QED_ALGO_BERENDS_GIELE = 1 } qed_algorithm;
+typedef struct {
+  int algorithm;
+  int variant;
+} qed_process_options;
+qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
+                                 const qed_process_options* options, qed_process** proc);
+
 /* Free a handle (NULL is a no-op).  Work already enqueued with it is unaffected. */
 qed_status qed_process_destroy(qed_process* proc);
 
@@ -130,6 +145,8 @@ typedef struct {
   int grid_blocks;           /* persistent grid size used for large batches */
   int64_t flops_per_point;   /* algorithmic FP64 flops per point (FMA = 2) */
   int64_t bytes_per_point;   /* algorithmic HBM bytes per point (momenta in + |M|^2 out) */
+  int algorithm;             /* qed_algorithm */
+  int variant;               /* launch variant in use */
 } qed_process_info;
 qed_status qed_get_process_info(const qed_process* proc, qed_process_info* info);
 

@@ -58,11 +58,13 @@ def _compile(src: str, force: bool) -> str:
 def build(force: bool = False, jobs: int | None = None) -> str:
     sys.path.insert(0, ROOT) if ROOT not in sys.path else None
     from paper_2511_19456_b200.gen.emit import generate_all
+    from paper_2511_19456_b200.gen.emit_bg import generate_bg
     from paper_2511_19456_b200.gen.emit_regs import generate_regs
 
     os.makedirs(OBJ_DIR, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
-    sources = generate_all(GEN_DIR) + generate_regs(GEN_DIR) + [os.path.join(CSRC, "qed_runtime.cu")]
+    sources = generate_all(GEN_DIR) + generate_regs(GEN_DIR) + generate_bg(GEN_DIR) + \
+        [os.path.join(CSRC, "qed_runtime.cu")]
     jobs = jobs or min(len(sources), max(1, os.cpu_count() or 1))
     # largest translation unit first
     sources.sort(key=lambda s: -os.path.getsize(s))

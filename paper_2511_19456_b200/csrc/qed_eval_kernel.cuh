@@ -79,6 +79,66 @@ struct Tasks {
   }
 };
 
+// ---- Berends-Giele current tasks (gen/lower_bg.py): descriptor = 8 ushort
+// [mask, out, parent_1, eps_1, ..., parent_K, eps_K, pad...]; node = sum_q V(eps_q, parent_q), then S(Q)
+template <class T>
+struct BGTasks {
+  template <int K, bool ROW>
+  static __device__ __forceinline__ spinor vsum(const double* b, const uint4& raw) {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+    double e[3];
+    ld_eps(b + d[3], e);
+    spinor acc = ROW ? eslash_row(e, ld_aos(b, d[2])) : eslash_col(e, ld_aos(b, d[2]));
+#pragma unroll
+    for (int q = 1; q < K; ++q) {
+      ld_eps(b + d[3 + 2 * q], e);
+      if (ROW) eslash_row_acc(e, ld_aos(b, d[2 + 2 * q]), acc);
+      else eslash_col_acc(e, ld_aos(b, d[2 + 2 * q]), acc);
+    }
+    return acc;
+  }
+  template <int K>
+  static __device__ __forceinline__ void in_node(double* b, uint4 raw) {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+    double m[5];
+    ld_mask(b + d[0], m);
+    st_aos(b, d[1], prop_col(m, vsum<K, false>(b, raw)));
+  }
+  template <int K>
+  static __device__ __forceinline__ void out_node(double* b, uint4 raw) {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+    double m[5];
+    ld_mask(b + d[0], m);
+    st_aos(b, d[1], prop_row(m, vsum<K, true>(b, raw)));
+  }
+  template <int K>
+  static __device__ __forceinline__ void in_leaf(double* b, uint4 raw) {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+    double m[5];
+    ld_mask(b + d[0], m);
+    st_leaf<T::NHI>(b, T::PHI, d[1], prop_col(m, vsum<K, false>(b, raw)));
+  }
+  template <int K>
+  static __device__ __forceinline__ void out_leaf(double* b, uint4 raw) {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+    st_leaf<T::NHO>(b, T::UBL, d[1], vsum<K, true>(b, raw));
+  }
+};
+
+template <class T, int COUNT, class F>
+__device__ __forceinline__ void run_tasks8(double* base, int g, const uint4* __restrict__ tbl, F f) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  uint4 d[TRIPS];
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k) {
+    const int t = g + k * T::G;
+    d[k] = (t < COUNT) ? tbl[t] : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k)
+    if (COUNT % T::G == 0 || g + k * T::G < COUNT) f(base, d[k]);
+}
+
 // run COUNT tasks of one kind over the G lanes of the group (compile-time trip count, descriptors
 // loaded up front so the table latency overlaps)
 template <class T, int COUNT, class F>
@@ -107,48 +167,38 @@ __device__ __forceinline__ void group_sync(int pb) {
 template <class T>
 __device__ __forceinline__ void stage_externals(double* base, int g, const QedEvalArgs& a) {
   constexpr int N = T::N;
-  constexpr int NT = N + 2 + (1 << N) - 2;
-  for (int t = g; t < NT; t += T::G) {
-    if (t < N) {
-      external_eps(base + T::MOM + 4 * ((a.photon_particle >> (4 * t)) & 15), base + T::EPS + 8 * t);
-    } else if (t == N) {
-      const double* p = base + T::MOM;
-      const double r = rsqrt(p[0] + 1.0), nn = (p[0] + 1.0) * r;
-      spinor u0, u1;   // u(p, s) = (n chi_s, sigma.p chi_s / n)
-      u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {p[3] * r, 0}; u0.v[3] = {p[1] * r, p[2] * r};
-      u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {p[1] * r, -p[2] * r}; u1.v[3] = {-p[3] * r, 0};
-      st_aos(base, T::U, u0);
-      st_aos(base, T::U + 8, u1);
-    } else if (t == N + 1) {
-      const double* p = base + T::MOM + 4 * a.e_out_particle;
-      const double r = rsqrt(p[0] + 1.0), nn = (p[0] + 1.0) * r;
-      spinor u0, u1;   // ubar(p', s') = u^dagger gamma^0
-      u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {-p[3] * r, 0}; u0.v[3] = {-p[1] * r, p[2] * r};
-      u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {-p[1] * r, -p[2] * r}; u1.v[3] = {p[3] * r, 0};
-      st_aos(base, T::UB, u0);
-      st_aos(base, T::UB + 8, u1);
-    } else {
-      // propagator constants of S(Q_S), Q_S = p + sum_{i in S} q_i, q = +k (in) / -k (out)
-      const int m = t - (N + 2) + 1;
-      double Q0 = base[T::MOM + 0], Q1 = base[T::MOM + 1], Q2 = base[T::MOM + 2], Q3 = base[T::MOM + 3];
+  constexpr int NM = (1 << N) - 2;
+  // propagator constants of S(Q_S) for every proper photon subset S = m (uniform loop, no divergence):
+  // Q_S = p + sum_{i in S} q_i, q = +k (in) / -k (out)
+  for (int t = g; t < NM; t += T::G) {
+    const int m = t + 1;
+    double Q0 = base[T::MOM + 0], Q1 = base[T::MOM + 1], Q2 = base[T::MOM + 2], Q3 = base[T::MOM + 3];
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        if ((m >> i) & 1) {
-          const double* k = base + T::MOM + 4 * ((a.photon_particle >> (4 * i)) & 15);
-          if (i < a.n_in_ph) {
-            Q0 += k[0]; Q1 += k[1]; Q2 += k[2]; Q3 += k[3];
-          } else {
-            Q0 -= k[0]; Q1 -= k[1]; Q2 -= k[2]; Q3 -= k[3];
-          }
-        }
-      }
-      const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;
-      const double inv = 1.0 / D;
-      double* mk = base + T::MASK + 6 * m;
-      reinterpret_cast<double2*>(mk)[0] = make_double2((Q0 + 1.0) * inv, (1.0 - Q0) * inv);
-      reinterpret_cast<double2*>(mk)[1] = make_double2(Q1 * inv, Q2 * inv);
-      reinterpret_cast<double2*>(mk)[2] = make_double2(Q3 * inv, 0.0);
+    for (int i = 0; i < N; ++i) {
+      const double* k = base + T::MOM + 4 * ((a.photon_particle >> (4 * i)) & 15);
+      const double w = ((m >> i) & 1) ? (i < a.n_in_ph ? 1.0 : -1.0) : 0.0;
+      Q0 = fma(w, k[0], Q0); Q1 = fma(w, k[1], Q1); Q2 = fma(w, k[2], Q2); Q3 = fma(w, k[3], Q3);
     }
+    const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;
+    const double inv = 1.0 / D;
+    double* mk = base + T::MASK + 6 * m;
+    reinterpret_cast<double2*>(mk)[0] = make_double2((Q0 + 1.0) * inv, (1.0 - Q0) * inv);
+    reinterpret_cast<double2*>(mk)[1] = make_double2(Q1 * inv, Q2 * inv);
+    reinterpret_cast<double2*>(mk)[2] = make_double2(Q3 * inv, 0.0);
+  }
+  // polarisation vectors
+  for (int t = g; t < N; t += T::G)
+    external_eps(base + T::MOM + 4 * ((a.photon_particle >> (4 * t)) & 15), base + T::EPS + 8 * t);
+  // electron spinors: lane 0 u(p, s), lane 1 ubar(p', s')
+  if (g < 2) {
+    const double* p = base + T::MOM + (g == 0 ? 0 : 4 * a.e_out_particle);
+    const double r = rsqrt(p[0] + 1.0), nn = (p[0] + 1.0) * r, sg = g == 0 ? 1.0 : -1.0;
+    // u(p, s) = (n chi_s, sigma.p chi_s / n);  ubar(p', s') = u^dagger gamma^0 (conjugated lower half negated)
+    spinor u0, u1;
+    u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {sg * p[3] * r, 0}; u0.v[3] = {sg * p[1] * r, p[2] * r};
+    u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {sg * p[1] * r, -p[2] * r}; u1.v[3] = {-sg * p[3] * r, 0};
+    st_aos(base, g == 0 ? T::U : T::UB, u0);
+    st_aos(base, (g == 0 ? T::U : T::UB) + 8, u1);
   }
 }
 

@@ -37,6 +37,26 @@ void qedgen_config_N3(int, int*, int*, long long*, long long*);
 void qedgen_config_N4(int, int*, int*, long long*, long long*);
 void qedgen_config_N5(int, int*, int*, long long*, long long*);
 void qedgen_config_N6(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N2(int, int);
+const void* qedbg_mc_kernel_N2(int);
+int qedbg_num_variants_N2(void);
+void qedbg_config_N2(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N3(int, int);
+const void* qedbg_mc_kernel_N3(int);
+int qedbg_num_variants_N3(void);
+void qedbg_config_N3(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N4(int, int);
+const void* qedbg_mc_kernel_N4(int);
+int qedbg_num_variants_N4(void);
+void qedbg_config_N4(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N5(int, int);
+const void* qedbg_mc_kernel_N5(int);
+int qedbg_num_variants_N5(void);
+void qedbg_config_N5(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N6(int, int);
+const void* qedbg_mc_kernel_N6(int);
+int qedbg_num_variants_N6(void);
+void qedbg_config_N6(int, int*, int*, long long*, long long*);
 const void* qedregs_kernel_N2(int, int);
 int qedregs_num_variants_N2(void);
 const void* qedregs_kernel_N3(int, int);
@@ -74,6 +94,14 @@ const KernelEntry kKernels[] = {
     {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6},
 };
 
+const KernelEntry kBGKernels[] = {
+    {qedbg_kernel_N2, qedbg_mc_kernel_N2, qedbg_config_N2, qedbg_num_variants_N2},
+    {qedbg_kernel_N3, qedbg_mc_kernel_N3, qedbg_config_N3, qedbg_num_variants_N3},
+    {qedbg_kernel_N4, qedbg_mc_kernel_N4, qedbg_config_N4, qedbg_num_variants_N4},
+    {qedbg_kernel_N5, qedbg_mc_kernel_N5, qedbg_config_N5, qedbg_num_variants_N5},
+    {qedbg_kernel_N6, qedbg_mc_kernel_N6, qedbg_config_N6, qedbg_num_variants_N6},
+};
+
 // launch variant from QED_VARIANT (tuning experiments); 0 = default, out-of-range -> 0
 int variant_from_env(int n_variants) {
   const char* v = getenv("QED_VARIANT");
@@ -89,7 +117,7 @@ struct qed_process {
   qed::QedEvalArgs args{};
   const void* kern[2] = {nullptr, nullptr};
   const void* kern_mc = nullptr;
-  int variant = 0;
+  int variant = 0, algorithm = 0;
   int wpb = 0, ppw = 0, grid_blocks = 0, mc_wpb = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
   long long smem = 0, smem_mc = 0, flops = 0;
   // staging for the host-buffer entry point
@@ -118,6 +146,11 @@ static qed_status check_spec(const qed_state_spec* s, const char* side) {
 
 qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
                               qed_process** proc) {
+  return qed_process_create_ex(in, out, n_photons, nullptr, proc);
+}
+
+qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
+                                 const qed_process_options* options, qed_process** proc) {
   if (!proc) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
   *proc = nullptr;
   qed_status st;
@@ -173,19 +206,27 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
     if (spin_of(j) < 0) norm *= 0.5;
   a.norm = norm;
 
-  const KernelEntry& ke = kKernels[N - 2];
+  const int algorithm = options ? options->algorithm : QED_ALGO_CDAG;
+  if (algorithm != QED_ALGO_CDAG && algorithm != QED_ALGO_BERENDS_GIELE) {
+    delete P;
+    return fail(QED_ERR_INVALID_ARGUMENT, "unknown algorithm");
+  }
+  P->algorithm = algorithm;
+  const KernelEntry& ke = algorithm == QED_ALGO_BERENDS_GIELE ? kBGKernels[N - 2] : kKernels[N - 2];
   // n = 1, 2: register-resident straight-line kernels (qed_eval_regs.cuh); n >= 3: lane-group
   // kernels with shared-memory trie staging (qed_eval_kernel.cuh).  QED_KERNEL=group forces the latter.
   const char* force = getenv("QED_KERNEL");
-  const bool use_regs = N <= 3 && !(force && strcmp(force, "group") == 0);
+  const bool use_regs = algorithm == QED_ALGO_CDAG && N <= 3 && !(force && strcmp(force, "group") == 0);
   if (use_regs) {
-    const int v = variant_from_env(N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3());
+    const int nv = N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3();
+    const int v = (options && options->variant >= 0 && options->variant < nv) ? options->variant : variant_from_env(nv);
     P->variant = v;
     P->kern[0] = N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
     P->kern[1] = N == 2 ? qedregs_kernel_N2(1, v) : qedregs_kernel_N3(1, v);
     (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
   } else {
-    const int v = variant_from_env(ke.num_variants());
+    const int nv = ke.num_variants();
+    const int v = (options && options->variant >= 0 && options->variant < nv) ? options->variant : variant_from_env(nv);
     P->variant = v;
     P->kern[0] = ke.kernel(0, v);
     P->kern[1] = ke.kernel(1, v);
@@ -342,6 +383,8 @@ qed_status qed_get_process_info(const qed_process* P, qed_process_info* info) {
   info->grid_blocks = P->grid_blocks;
   info->flops_per_point = P->flops;
   info->bytes_per_point = 8LL * (4 * P->n_ext + 1);
+  info->algorithm = P->algorithm;
+  info->variant = P->variant;
   return QED_OK;
 }
 

@@ -143,3 +143,92 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
             hx |= ((h >> (1 + i)) & 1) << photon_particle[i]
         out[hx] = e_n * amp[h]
     return out
+
+
+def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
+    """Berends-Giele plan (gen/lower_bg.py) executed with the device layout; returns amplitudes
+    in external bit order with e^N (same contract as eval_point)."""
+    N, L = plan.N, plan.layout
+    sm = np.zeros(plan.stride + 8)
+
+    def put_aos(off, v):
+        for c in range(4):
+            o = aos_slot(off, c)
+            sm[o], sm[o + 1] = v[c].real, v[c].imag
+
+    def get_aos(off):
+        return np.array([complex(sm[aos_slot(off, c)], sm[aos_slot(off, c) + 1]) for c in range(4)])
+
+    def put_leaf(base, nh, h, v):
+        for c in range(4):
+            o = base + (c * nh + swz(h)) * 2
+            sm[o], sm[o + 1] = v[c].real, v[c].imag
+
+    def get_leaf(base, nh, h):
+        return np.array([complex(sm[base + (c * nh + swz(h)) * 2], sm[base + (c * nh + swz(h)) * 2 + 1])
+                         for c in range(4)])
+
+    photon_particle = [1 + i if i < n_in_ph else n_in_ph + 2 + (i - n_in_ph) for i in range(N)]
+    sign = [1.0 if i < n_in_ph else -1.0 for i in range(N)]
+    p, pp = mom[0], mom[n_in_ph + 1]
+    for i in range(N):
+        k = mom[photon_particle[i]]
+        kperp = math.hypot(k[1], k[2])
+        kn = math.sqrt(kperp * kperp + k[3] * k[3])
+        ct, st = k[3] / kn, kperp / kn
+        cf, sf = (k[1] / kperp, k[2] / kperp) if kperp > 0 else (1.0, 0.0)
+        sm[L["EPS"] + i * 8: L["EPS"] + i * 8 + 3] = (ct * cf, ct * sf, -st)
+        sm[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
+    n = math.sqrt(p[0] + 1)
+    put_aos(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
+    put_aos(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
+    n = math.sqrt(pp[0] + 1)
+    put_aos(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
+    put_aos(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
+    for m in range(1, (1 << N) - 1):
+        Q = p.copy()
+        for i in range(N):
+            if m >> i & 1:
+                Q = Q + sign[i] * mom[photon_particle[i]]
+        inv = 1 / (Q[0] ** 2 - Q[1] ** 2 - Q[2] ** 2 - Q[3] ** 2 - 1)
+        sm[L["MASK"] + m * 6: L["MASK"] + m * 6 + 5] = ((Q[0] + 1) * inv, (1 - Q[0]) * inv,
+                                                        Q[1] * inv, Q[2] * inv, Q[3] * inv)
+
+    def vsum(d, row):
+        K = (len(d) - 2) // 2
+        acc = np.zeros(4, complex)
+        for q in range(K):
+            par, e = d[2 + 2 * q], d[3 + 2 * q]
+            f = _eslash_row if row else _eslash_col
+            acc = acc + f(sm[e: e + 3], get_aos(par))
+        return acc
+
+    for kind, K, tasks in plan.levels:
+        for d in tasks:
+            if kind == "in":
+                put_aos(d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
+            else:
+                put_aos(d[1], _prop_row(sm[d[0]: d[0] + 5], vsum(d, True)))
+    H = plan.H
+    amp = np.zeros(H, dtype=complex)
+    for si, A in enumerate(plan.sets):
+        for d in plan.set_in[si]:
+            put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
+        for d in plan.set_out[si]:
+            put_leaf(L["UBL"], plan.n_ho, d[1], vsum(d, True))
+        Ac = [x for x in range(N) if x not in A]
+        pos = plan.set_pos[si]
+        for h in range(H):
+            s, sp = h & 1, (h >> (N + 1)) & 1
+            hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
+            ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
+            amp[h] += get_leaf(L["UBL"], plan.n_ho, ho) @ get_leaf(L["PHI"], plan.n_hi, hi)
+    e_n = math.sqrt(4 * math.pi * ALPHA) ** N
+    out = np.zeros(H, dtype=complex)
+    e_out = n_in_ph + 1
+    for h in range(H):
+        hx = (h & 1) | (((h >> (N + 1)) & 1) << e_out)
+        for i in range(N):
+            hx |= ((h >> (1 + i)) & 1) << photon_particle[i]
+        out[hx] = e_n * amp[h]
+    return out

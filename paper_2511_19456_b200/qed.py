@@ -19,7 +19,7 @@ MC_CHUNK = 8192
 _STATUS = {0: "QED_OK", 1: "QED_ERR_INVALID_ARGUMENT", 2: "QED_ERR_UNSUPPORTED", 3: "QED_ERR_CUDA",
            4: "QED_ERR_OUT_OF_MEMORY", 5: "QED_ERR_INTERNAL"}
 
-EXPORTED = ["qed_process_create", "qed_process_destroy", "qed_eval_msq", "qed_eval_msq_configs",
+EXPORTED = ["qed_process_create", "qed_process_create_ex", "qed_process_destroy", "qed_eval_msq", "qed_eval_msq_configs",
             "qed_eval_msq_host", "qed_mc_sum", "qed_get_process_info", "qed_last_error", "qed_launch_count"]
 
 
@@ -38,11 +38,19 @@ class _McConfig(ctypes.Structure):
                 ("first_index", ctypes.c_uint64), ("n_points", ctypes.c_uint64)]
 
 
+class _Options(ctypes.Structure):
+    _fields_ = [("algorithm", ctypes.c_int), ("variant", ctypes.c_int)]
+
+
+ALGORITHMS = {"cdag": 0, "bg": 1, "berends-giele": 1}
+
+
 class ProcessInfo(ctypes.Structure):
     _fields_ = [("n_photons", ctypes.c_int), ("n_ext", ctypes.c_int), ("n_configs", ctypes.c_int),
                 ("n_diagrams", ctypes.c_int), ("lanes_per_point", ctypes.c_int), ("warps_per_block", ctypes.c_int),
                 ("smem_per_block", ctypes.c_int64), ("grid_blocks", ctypes.c_int),
-                ("flops_per_point", ctypes.c_int64), ("bytes_per_point", ctypes.c_int64)]
+                ("flops_per_point", ctypes.c_int64), ("bytes_per_point", ctypes.c_int64),
+                ("algorithm", ctypes.c_int), ("variant", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -56,6 +64,8 @@ def _load() -> ctypes.CDLL:
     vp, i64 = ctypes.c_void_p, ctypes.c_int64
     lib.qed_process_create.argtypes = [ctypes.POINTER(_Spec), ctypes.POINTER(_Spec), ctypes.c_int,
                                        ctypes.POINTER(vp)]
+    lib.qed_process_create_ex.argtypes = [ctypes.POINTER(_Spec), ctypes.POINTER(_Spec), ctypes.c_int,
+                                          ctypes.POINTER(_Options), ctypes.POINTER(vp)]
     lib.qed_process_destroy.argtypes = [vp]
     lib.qed_eval_msq.argtypes = [vp, vp, i64, vp, vp]
     lib.qed_eval_msq_configs.argtypes = [vp, vp, i64, vp, vp]
@@ -108,9 +118,12 @@ def _ptr(t, n_min: int, name: str) -> int:
 
 class Process:
     """qed_process handle.  ``in_spins`` / ``out_spins``: None (all summed) or a list
-    [electron, photon...] of -1 (summed) / 0 / 1 (fixed)."""
+    [electron, photon...] of -1 (summed) / 0 / 1 (fixed).  ``algorithm``: "cdag" (the paper's
+    node-reduced diagram DAG, default) or "bg" (Berends-Giele distributive rewrite); ``variant``:
+    launch variant (None = default / QED_VARIANT)."""
 
-    def __init__(self, n: int, n_in_photons: int = 1, in_spins=None, out_spins=None):
+    def __init__(self, n: int, n_in_photons: int = 1, in_spins=None, out_spins=None, algorithm: str = "cdag",
+                 variant: int | None = None):
         self.n = n
         self.n_in_photons = n_in_photons
         self.n_out_photons = n + 1 - n_in_photons
@@ -131,8 +144,12 @@ class Process:
         self._in = spec(n_in_photons, in_spins)
         self._out = spec(self.n_out_photons, out_spins)
         h = ctypes.c_void_p()
-        _check(_lib.qed_process_create(ctypes.byref(self._in), ctypes.byref(self._out), n, ctypes.byref(h)),
-               "qed_process_create")
+        if algorithm not in ALGORITHMS:
+            raise ValueError(f"algorithm must be one of {sorted(ALGORITHMS)}")
+        self.algorithm = algorithm
+        opt = _Options(ALGORITHMS[algorithm], -1 if variant is None else int(variant))
+        _check(_lib.qed_process_create_ex(ctypes.byref(self._in), ctypes.byref(self._out), n, ctypes.byref(opt),
+                                          ctypes.byref(h)), "qed_process_create_ex")
         self._h = h
 
     def close(self):

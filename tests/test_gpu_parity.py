@@ -190,3 +190,47 @@ def test_two_streams_two_handles(qed):
     ref2 = oracle.msq(1, n, mom[:500].numpy(), spec=[0, -1, -1, -1, -1])
     assert np.max(np.abs(o1[:500].cpu().numpy() / ref1 - 1)) <= TOL
     assert np.max(np.abs(o2[:500].cpu().numpy() / ref2 - 1)) <= TOL
+
+
+# ---------------------------------------------------------------- Berends-Giele kernels (QED_ALGO_BERENDS_GIELE)
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_bg_averaged_msq_matches_oracle(qed, n):
+    mom = synthetic.rambo_cm(n, PARITY_POINTS[n], sqrt_s=5.0, seed=1100 + n)
+    got = _gpu_msq(qed, qed.Process(n, algorithm="bg"), mom)
+    ref = oracle.msq(1, n, mom.numpy())
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_bg_per_configuration_matches_oracle(qed, n):
+    npts = min(PARITY_POINTS[n], 257)
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=2100 + n)
+    got = _gpu_configs(qed, qed.Process(n, algorithm="bg"), mom)
+    ref = np.abs(oracle.amps(1, n, mom.numpy())) ** 2
+    assert np.max(np.abs(got - ref) / ref.max(axis=1, keepdims=True)) <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_bg_paper_direction_and_fixed_states(qed, n):
+    mom = synthetic.rambo_cm(n, 129, sqrt_s=5.0, seed=4100 + n).numpy()
+    rev = np.concatenate([mom[:, 2:3], mom[:, 3:], mom[:, 0:1], mom[:, 1:2]], axis=1)
+    got = _gpu_msq(qed, qed.Process(n, n_in_photons=n, algorithm="bg"), torch.from_numpy(rev))
+    assert np.max(np.abs(got / oracle.msq(n, 1, rev) - 1)) <= TOL
+    spec = [0, -1, 1] + [-1] * n
+    got = _gpu_msq(qed, qed.Process(n, in_spins=spec[:2], out_spins=spec[2:], algorithm="bg"), torch.from_numpy(mom))
+    ref = oracle.msq(1, n, mom, spec=spec)
+    assert np.max(np.abs(got - ref) / oracle.msq(1, n, mom)) <= TOL
+
+
+@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 1024), (5, 1 << 18, 24)])
+def test_bg_full_size_sampled(qed, n, npts, sample):
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=7100 + n, device="cuda")
+    out = torch.empty(npts, dtype=torch.float64, device="cuda")
+    qed.Process(n, algorithm="bg").eval_msq(synthetic.to_soa(mom), out)
+    torch.cuda.synchronize()
+    idx = torch.cat([torch.tensor([0, npts - 1]), torch.randint(0, npts, (sample,))]).unique()
+    got = out[idx.cuda()].cpu().numpy()
+    ref = oracle.msq(1, n, mom[idx.cuda()].cpu().numpy())
+    assert np.all(np.isfinite(out.cpu().numpy()))
+    assert np.max(np.abs(got / ref - 1)) <= TOL

@@ -148,13 +148,14 @@ MC_CASES = [(1, 20000, 0, 0.0), (2, 12000, 5000, 0.25), (3, 2500, 8000, 0.25), (
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("algorithm", ["cdag", "bg"])
 @pytest.mark.parametrize("n,count,first,omega_min", MC_CASES)
-def test_gpu_mc_sum_matches_oracle(n, count, first, omega_min):
+def test_gpu_mc_sum_matches_oracle(n, count, first, omega_min, algorithm):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2511_19456_b200 import qed
     sqrt_s, seed = 5.0, 1234 + n
-    proc = qed.Process(n)
+    proc = qed.Process(n, algorithm=algorithm)
     nch = mc.n_chunks(first + count)
     partials = torch.zeros(3 * nch, dtype=torch.float64, device="cuda")
     proc.mc_sum(partials, sqrt_s, omega_min, seed, first, count)
