@@ -125,34 +125,57 @@ struct BGTasks {
   }
 };
 
-template <class T, int COUNT, class F>
+// task functors (always inlined; passed as template arguments by the generated schedules)
+template <class T, int KIND>
+struct TaskFn {  // KIND: 0 vs_col, 1 vs_row, 2 phi, 3 ub
+  __device__ __forceinline__ void operator()(double* b, ushort4 d) const {
+    if (KIND == 0) Tasks<T>::vs_col(b, d);
+    else if (KIND == 1) Tasks<T>::vs_row(b, d);
+    else if (KIND == 2) Tasks<T>::phi(b, d);
+    else Tasks<T>::ub(b, d);
+  }
+};
+template <class T, int K, int KIND>
+struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
+  __device__ __forceinline__ void operator()(double* b, uint4 d) const {
+    if (KIND == 0) BGTasks<T>::template in_node<K>(b, d);
+    else if (KIND == 1) BGTasks<T>::template out_node<K>(b, d);
+    else if (KIND == 2) BGTasks<T>::template in_leaf<K>(b, d);
+    else BGTasks<T>::template out_leaf<K>(b, d);
+  }
+};
+
+// OFF: lane offset, so that two task kinds of one stage occupy different lanes / warps
+template <class T, int COUNT, class F, int OFF = 0>
 __device__ __forceinline__ void run_tasks8(double* base, int g, const uint4* __restrict__ tbl, F f) {
   constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
   uint4 d[TRIPS];
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k) {
-    const int t = g + k * T::G;
+    const int t = gl + k * T::G;
     d[k] = (t < COUNT) ? tbl[t] : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k)
-    if (COUNT % T::G == 0 || g + k * T::G < COUNT) f(base, d[k]);
+    if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
 }
 
 // run COUNT tasks of one kind over the G lanes of the group (compile-time trip count, descriptors
 // loaded up front so the table latency overlaps)
-template <class T, int COUNT, class F>
+template <class T, int COUNT, class F, int OFF = 0>
 __device__ __forceinline__ void run_tasks(double* base, int g, const ushort4* __restrict__ tbl, F f) {
   constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
   ushort4 d[TRIPS];
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k) {
-    const int t = g + k * T::G;
+    const int t = gl + k * T::G;
     d[k] = (t < COUNT) ? tbl[t] : make_ushort4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k)
-    if (COUNT % T::G == 0 || g + k * T::G < COUNT) f(base, d[k]);
+    if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
 }
 
 template <class T>

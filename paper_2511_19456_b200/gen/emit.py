@@ -48,6 +48,15 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     return [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
 
 
+def lane_offset(count_first: int, G: int) -> int:
+    """Start lane of the second task kind of a stage: right after the first kind's last lane,
+    rounded up to a warp boundary when the group spans several warps (no intra-warp divergence)."""
+    off = count_first % G
+    if G > 32 and off:
+        off = ((off + 31) // 32 * 32) % G
+    return off
+
+
 def _tasks(name, tasks):
     if not tasks:
         return f"__device__ const ushort4 {name}[1] = {{{{0, 0, 0, 0}}}};\n"
@@ -69,13 +78,13 @@ def emit_source(plan: Plan) -> str:
     for lv in range(max(len(plan.in_levels), len(plan.out_levels))):
         if lv < len(plan.in_levels):
             t = plan.in_levels[lv]
-            lines.append(f"    qed::run_tasks<T, {len(t)}>(base, g, k_in_tasks + {len(in_flat)}, "
-                         "[](double* b, ushort4 d) { qed::Tasks<T>::vs_col(b, d); });")
+            lines.append(f"    qed::run_tasks<T, {len(t)}>(base, g, k_in_tasks + {len(in_flat)}, qed::TaskFn<T, 0>{{}});")
             in_flat += t
         if lv < len(plan.out_levels):
             t = plan.out_levels[lv]
-            lines.append(f"    qed::run_tasks<T, {len(t)}>(base, g, k_out_tasks + {len(out_flat)}, "
-                         "[](double* b, ushort4 d) { qed::Tasks<T>::vs_row(b, d); });")
+            off = lane_offset(len(plan.in_levels[lv]), plan.G) if lv < len(plan.in_levels) else 0
+            lines.append(f"    qed::run_tasks<T, {len(t)}, qed::TaskFn<T, 1>, {off}>(base, g, k_out_tasks + {len(out_flat)}, "
+                         "qed::TaskFn<T, 1>{});")
             out_flat += t
         lines.append("    qed::group_sync<T>(pb);")
     interiors = "\n".join(lines) if lines else "    (void)base; (void)g; (void)pb;"
@@ -92,10 +101,14 @@ def emit_source(plan: Plan) -> str:
     for i, st in enumerate(struct):
         if i > 0:
             lines.append("    qed::group_sync<T>(pb);")
-        for kind, cnt in st:
-            lines.append(f"    qed::run_tasks<T, {cnt}>(base, g, k_set_tasks + si * {per_set} + {off}, "
-                         f"[](double* b, ushort4 d) {{ qed::Tasks<T>::{KIND_FN[kind]}(b, d); }});")
+        prev = 0
+        for q, (kind, cnt) in enumerate(st):
+            lo = lane_offset(prev, plan.G) if q > 0 else 0
+            kid = {"vs_col": 0, "vs_row": 1, "phi": 2, "ub": 3}[kind]
+            lines.append(f"    qed::run_tasks<T, {cnt}, qed::TaskFn<T, {kid}>, {lo}>(base, g, "
+                         f"k_set_tasks + si * {per_set} + {off}, qed::TaskFn<T, {kid}>{{}});")
             off += cnt
+            prev = cnt
     run_set = "\n".join(lines)
     set_pos = [p for ps in plan.set_pos for p in ps]
     set_mask = [sum(1 << x for x in A) for A in plan.sets]

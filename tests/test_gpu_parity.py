@@ -234,3 +234,50 @@ def test_bg_full_size_sampled(qed, n, npts, sample):
     ref = oracle.msq(1, n, mom[idx.cuda()].cpu().numpy())
     assert np.all(np.isfinite(out.cpu().numpy()))
     assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+# ---------------------------------------------------------------- stress kinematics (SURVEY.md §8(d) "Stress")
+
+@pytest.mark.parametrize("algorithm", ["cdag", "bg"])
+@pytest.mark.parametrize("n,sqrt_s", [(2, 1.5), (2, 20.0), (2, 100.0), (2, 1000.0), (3, 1.5), (3, 100.0), (4, 20.0)])
+def test_extreme_energies(qed, n, sqrt_s, algorithm):
+    mom = synthetic.rambo_cm(n, 257, sqrt_s=sqrt_s, seed=int(8000 + 10 * n + sqrt_s))
+    got = _gpu_msq(qed, qed.Process(n, algorithm=algorithm), mom)
+    ref = oracle.msq(1, n, mom.numpy(), kind="f80")     # long-double oracle: conditioning reference
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+@pytest.mark.parametrize("algorithm", ["cdag", "bg"])
+def test_photons_along_the_beam_axis(qed, algorithm):
+    """k_perp = 0 (phi := 0 reading, R6): n = 1 in the CM frame with the outgoing photon
+    exactly along -z (backscatter) and +z (forward), n = 2 with one photon along -z."""
+    s5 = 5.0
+    kin = (s5 * s5 - 1) / (2 * s5)
+    e_in = np.array([(s5 * s5 + 1) / (2 * s5), 0, 0, -kin])
+    g_in = np.array([kin, 0, 0, kin])
+    pts = []
+    for sgn in (-1.0, 1.0):
+        g_out = np.array([kin, 0, 0, sgn * kin])
+        pts.append([e_in, g_in, e_in + g_in - g_out, g_out])
+    mom = torch.tensor(np.array(pts))
+    got = _gpu_msq(qed, qed.Process(1, algorithm=algorithm), mom)
+    ref = oracle.msq(1, 1, mom.numpy())
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+    base = synthetic.rambo_cm(2, 16, sqrt_s=s5, seed=77).numpy()
+    # rotate each point so that the first outgoing photon lies along -z (exact zeros in k_x, k_y)
+    for p in base:
+        k = p[3, 1:]
+        kn = np.linalg.norm(k)
+        ax = np.cross(k / kn, [0, 0, -1.0])
+        sa = np.linalg.norm(ax)
+        ca = np.dot(k / kn, [0, 0, -1.0])
+        ax = ax / sa
+        K = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+        R = np.eye(3) + sa * K + (1 - ca) * K @ K
+        p[:, 1:] = p[:, 1:] @ R.T
+        p[3, 1:] = [0.0, 0.0, -kn]
+        p[2] = p[0] + p[1] - p[3] - p[4]     # restore exact conservation
+    got = _gpu_msq(qed, qed.Process(2, algorithm=algorithm), torch.from_numpy(base))
+    ref = oracle.msq(1, 2, base)
+    assert np.max(np.abs(got / ref - 1)) <= TOL

@@ -6,12 +6,15 @@ SPEC=${2:-"2:0,1,2,3,4 1:0,1,2,3,4 3:0,1,2 4:0,1,2 5:0,1,2"}
 OUT=gpurun_out/sweep_${TAG}.jsonl
 mkdir -p gpurun_out; : > $OUT
 declare -A PTS=([1]=4194304 [2]=4194304 [3]=2097152 [4]=1048576 [5]=262144)
+# item "n:variants" (CDAG) or "bgN:variants" (Berends-Giele)
 for item in $SPEC; do
-  n=${item%%:*}; vs=${item#*:}
+  key=${item%%:*}; vs=${item#*:}
+  algo=cdag; n=$key
+  if [[ $key == bg* ]]; then algo=bg; n=${key#bg}; fi
   for v in ${vs//,/ }; do
     QED_VARIANT=$v timeout 300 python bench.py --n $n --points ${PTS[$n]} --steps 10 --warmup 3 --no-per-n \
-      --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | \
-      python -c "import json,sys; d=json.loads(sys.stdin.read()); print(json.dumps({'n':$n,'variant':$v,'value':d['value'],'frac':d['roofline']['frac'],'sm_mhz':d['clocks']['sm_mhz'],'kernel':d['config']['kernel']}))" >> $OUT
+      --no-cpu-baseline --no-e2e --algorithm $algo 2>/dev/null | tail -1 | \
+      python -c "import json,sys; d=json.loads(sys.stdin.read()); print(json.dumps({'n':$n,'algorithm':'$algo','variant':$v,'value':d['value'],'frac':d['roofline']['frac'],'sm_mhz':d['clocks']['sm_mhz'],'kernel':d['config']['kernel']}))" >> $OUT
   done
 done
 cat $OUT
