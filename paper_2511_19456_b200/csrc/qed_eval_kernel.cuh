@@ -111,17 +111,18 @@ struct BGTasks {
     ld_mask(b + d[0], m);
     st_aos(b, d[1], prop_row(m, vsum<K, true>(b, raw)));
   }
+  // leaf descriptor field out = lb * 1024 + h: helicity h of the lb-th subset of the batch
   template <int K>
   static __device__ __forceinline__ void in_leaf(double* b, uint4 raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
-    st_leaf<T::NHI>(b, T::PHI, d[1], prop_col(m, vsum<K, false>(b, raw)));
+    st_leaf<T::NHI>(b + (d[1] >> 10) * T::LEAFB, T::PHI, d[1] & 1023, prop_col(m, vsum<K, false>(b, raw)));
   }
   template <int K>
   static __device__ __forceinline__ void out_leaf(double* b, uint4 raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
-    st_leaf<T::NHO>(b, T::UBL, d[1], vsum<K, true>(b, raw));
+    st_leaf<T::NHO>(b + (d[1] >> 10) * T::LEAFB, T::UBL, d[1] & 1023, vsum<K, true>(b, raw));
   }
 };
 
@@ -230,8 +231,9 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
 // phi of one sigma stays in registers across the tau loop; loops are rolled so that ptxas
 // cannot hoist every leaf load of the subset (which spills).
 template <class T, int AS>
-__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[AS][8]) {
+__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[AS][8], int lb = 0) {
   const int h0 = 2 * swz(hi), h1 = 2 * swz(hi + 1), o0 = 2 * swz(ho), o1 = 2 * swz(ho + 1);
+  base += lb * T::LEAFB;   // leaf buffer of the lb-th subset of a batch (T::SETB subsets per stage)
 #pragma unroll 1
   for (int sg = 0; sg < T::NSIG; ++sg) {
     c2 p0[4], p1[4];
@@ -280,18 +282,22 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
 #pragma unroll 1
-  for (int si = 0; si < T::NSETS; ++si) {
-    T::run_set(base, g, pb, si);
+  for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
+    T::run_set(base, g, pb, s0);      // leaves of subsets s0 .. s0 + SETB - 1
     group_sync<T>(pb);
-    int hi = 0, ho = 0;
-    const unsigned inA = T::set_mask(si);
 #pragma unroll
-    for (int i = 0; i < T::N; ++i) {
-      const int lam = (g >> i) & 1;
-      if ((inA >> i) & 1) hi |= lam << T::set_pos(si, i);
-      else ho |= lam << T::set_pos(si, i);
+    for (int lb = 0; lb < T::SETB; ++lb) {
+      const int si = s0 + lb;
+      int hi = 0, ho = 0;
+      const unsigned inA = T::set_mask(si);
+#pragma unroll
+      for (int i = 0; i < T::N; ++i) {
+        const int lam = (g >> i) & 1;
+        if ((inA >> i) & 1) hi |= lam << T::set_pos(si, i);
+        else ho |= lam << T::set_pos(si, i);
+      }
+      join_set<T, AS>(base, hi, ho, acc, lb);
     }
-    join_set<T, AS>(base, hi, ho, acc);
     group_sync<T>(pb);
   }
 #pragma unroll

@@ -149,7 +149,7 @@ struct T {{
   static constexpr int STRIDE = {plan.stride};
   static constexpr int {lay};
   static constexpr int NSIG = {plan.n_sigma}, NTAU = {plan.n_tau}, NHI = {plan.n_hi}, NHO = {plan.n_ho};
-  static constexpr int NSETS = {len(plan.sets)};
+  static constexpr int NSETS = {len(plan.sets)}, SETB = 1, LEAFB = 0;
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}

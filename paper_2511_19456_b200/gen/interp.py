@@ -159,12 +159,17 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     def get_aos(off):
         return np.array([complex(sm[aos_slot(off, c)], sm[aos_slot(off, c) + 1]) for c in range(4)])
 
-    def put_leaf(base, nh, h, v):
+    LB = L["LEAFB"]
+
+    def put_leaf(base, nh, hx, v):
+        base += (hx >> 10) * LB
+        h = hx & 1023
         for c in range(4):
             o = base + (c * nh + swz(h)) * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
-    def get_leaf(base, nh, h):
+    def get_leaf(base, nh, h, lb=0):
+        base += lb * LB
         return np.array([complex(sm[base + (c * nh + swz(h)) * 2], sm[base + (c * nh + swz(h)) * 2 + 1])
                          for c in range(4)])
 
@@ -212,17 +217,20 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     H = plan.H
     amp = np.zeros(H, dtype=complex)
     for si, A in enumerate(plan.sets):
-        for d in plan.set_in[si]:
-            put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
-        for d in plan.set_out[si]:
-            put_leaf(L["UBL"], plan.n_ho, d[1], vsum(d, True))
+        lb = si % plan.setb
+        if lb == 0:
+            for sj in range(si, si + plan.setb):
+                for d in plan.set_in[sj]:
+                    put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
+                for d in plan.set_out[sj]:
+                    put_leaf(L["UBL"], plan.n_ho, d[1], vsum(d, True))
         Ac = [x for x in range(N) if x not in A]
         pos = plan.set_pos[si]
         for h in range(H):
             s, sp = h & 1, (h >> (N + 1)) & 1
             hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
             ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
-            amp[h] += get_leaf(L["UBL"], plan.n_ho, ho) @ get_leaf(L["PHI"], plan.n_hi, hi)
+            amp[h] += get_leaf(L["UBL"], plan.n_ho, ho, lb) @ get_leaf(L["PHI"], plan.n_hi, hi, lb)
     e_n = math.sqrt(4 * math.pi * ALPHA) ** N
     out = np.zeros(H, dtype=complex)
     e_out = n_in_ph + 1

@@ -69,12 +69,24 @@ def _subsets(N, k):
     return list(itertools.combinations(range(N), k))
 
 
-def make_bg_plan(N: int, j: int | None = None) -> BGPlan:
+def default_setb(N: int, j: int) -> int:
+    """Subsets per leaf stage: enough leaf tasks to fill the G = 2^N lanes of the group."""
+    n_sets = math.comb(N, j)
+    leaf_tasks = (1 << (j + 1)) + (1 << (N - j + 1))
+    b = 1
+    while b * 2 <= n_sets and n_sets % (b * 2) == 0 and b * leaf_tasks < (1 << N):
+        b *= 2
+    return b
+
+
+def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
     G = 1 << N
     full = (1 << N) - 1
+    if setb is None:
+        setb = default_setb(N, j)
     lay: dict[str, int] = {}
     off = 0
 
@@ -101,8 +113,11 @@ def make_bg_plan(N: int, j: int | None = None) -> BGPlan:
         alloc(f"OUT{k}", len(subs) * (1 << (k + 1)) * 8, 8)
         out_idx[k] = {s: i for i, s in enumerate(subs)}
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
+    leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL)
     alloc("PHI", 4 * n_hi * 2, 8)
     alloc("UBL", 4 * n_ho * 2, 8)
+    alloc("LEAFX", leafb * (setb - 1) - (lay["UBL"] + 4 * n_ho * 2 - lay["PHI"] - leafb) if setb > 1 else 0, 8)
+    lay["LEAFB"] = leafb
     stride = (off + 1) // 2 * 2
     if (stride // 2) % 2 == 0:
         stride += 2
@@ -139,6 +154,7 @@ def make_bg_plan(N: int, j: int | None = None) -> BGPlan:
         return d
 
     plan = BGPlan(N=N, j=j, G=G, sets=[], layout=lay, stride=stride)
+    plan.setb = setb
     for k in range(1, max(j, N - j)):
         if k < j:
             t = [task("in", S, h, node_off("in", S, h), mask_off(msk(S)))
@@ -157,8 +173,9 @@ def make_bg_plan(N: int, j: int | None = None) -> BGPlan:
         for k, x in enumerate(Ac):
             pos[x] = 1 + k
         plan.set_pos.append(pos)
-        plan.set_in.append([task("in", A, h, h, mask_off(msk(A))) for h in range(n_hi)])
-        plan.set_out.append([task("out", Ac, h, h, 0) for h in range(n_ho)])
+        lb = (len(plan.sets) - 1) % setb          # leaf buffer of this subset within its batch
+        plan.set_in.append([task("in", A, h, lb * 1024 + h, mask_off(msk(A))) for h in range(n_hi)])
+        plan.set_out.append([task("out", Ac, h, lb * 1024 + h, 0) for h in range(n_ho)])
 
     F = FLOPS_BG
     H = 1 << (N + 2)
