@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 METRIC = "|M|^2 evals/sec (phase-space pts/s) e-gamma->e-+n gamma"
 UNIT = "points/s"
 FP64_PEAK_TFLOPS = 148 * 128 * 1.965e9 / 1e12   # 148 SM x 64 DFMA/clk x 2 flop x 1965 MHz
-PER_N_POINTS = {1: 1 << 22, 2: 1 << 22, 3: 1 << 21, 4: 1 << 20, 5: 1 << 18}
+PER_N_POINTS = {1: 1 << 22, 2: 1 << 22, 3: 1 << 21, 4: 1 << 20, 5: 1 << 18, 6: 1 << 18, 7: 1 << 16, 8: 1 << 14}
 
 
 def parse():
@@ -245,8 +245,8 @@ def sweep_per_n(args, world, stream, dev, algorithm: str) -> dict:
     import synthetic
     from paper_2511_19456_b200 import qed
     out = {}
-    for m in range(1, 6):
-        Pm = PER_N_POINTS[m] * (4 if algorithm == "bg" and m >= 4 else 1)
+    for m in range(1, 9 if algorithm == "bg" else 6):
+        Pm = PER_N_POINTS[m] * (4 if algorithm == "bg" and 4 <= m <= 5 else 1)
         pm = qed.Process(m, algorithm=algorithm)
         mm = synthetic.rambo_cm(m, Pm, sqrt_s=args.sqrt_s, seed=7 + m, device=dev)
         sm = synthetic.to_soa(mm)

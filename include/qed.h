@@ -39,7 +39,7 @@ extern "C" {
 typedef enum {
   QED_OK = 0,
   QED_ERR_INVALID_ARGUMENT = 1, /* NULL handle/pointer, negative size, malformed spec */
-  QED_ERR_UNSUPPORTED = 2,      /* photon count outside 1 <= n <= 5, not an e- line process */
+  QED_ERR_UNSUPPORTED = 2,      /* photon count outside 1 <= n <= 5 (CDAG) / 1 <= n <= 8 (Berends-Giele) */
   QED_ERR_CUDA = 3,             /* a CUDA runtime call or kernel launch failed */
   QED_ERR_OUT_OF_MEMORY = 4,
   QED_ERR_INTERNAL = 5
@@ -62,7 +62,8 @@ typedef struct qed_process qed_process; /* opaque, owned by libqed */
 
 /* Create the handle for e- + in->n_photons gamma -> e- + out->n_photons gamma.
    n_photons is the paper's n: the total photon count minus one, i.e.
-   in->n_photons + out->n_photons == n_photons + 1, 1 <= n_photons <= 5.
+   in->n_photons + out->n_photons == n_photons + 1, 1 <= n_photons <= 5 (n <= 8 with
+   qed_process_create_ex(..., QED_ALGO_BERENDS_GIELE)).
    North-star process e- gamma -> e- + n gamma: in = {1, ...}, out = {n, ...}.
    Paper process e- gamma^n -> e- gamma: in = {n, ...}, out = {1, ...}.
    No device work; selects the generated kernel for N = n+1 photons on the current device.

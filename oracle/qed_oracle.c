@@ -47,7 +47,7 @@
 typedef ORACLE_REAL real;
 typedef ORACLE_REAL _Complex cplx;
 
-#define MAX_PHOTONS 8
+#define MAX_PHOTONS 9
 #define MAX_EXT (MAX_PHOTONS + 2)
 
 /* electron mass and fine-structure constant (CODATA 2018). */

@@ -79,12 +79,17 @@ struct Tasks {
   }
 };
 
-// ---- Berends-Giele current tasks (gen/lower_bg.py): descriptor = 8 ushort
+// ---- Berends-Giele current tasks (gen/lower_bg.py): descriptor = T::DW ushort (8 or 16)
 // [mask, out, parent_1, eps_1, ..., parent_K, eps_K, pad...]; node = sum_q V(eps_q, parent_q), then S(Q)
+template <int DW>
+struct Desc {
+  uint4 v[DW / 8];
+};
 template <class T>
 struct BGTasks {
+  using D = Desc<T::DW>;
   template <int K, bool ROW>
-  static __device__ __forceinline__ spinor vsum(const double* b, const uint4& raw) {
+  static __device__ __forceinline__ spinor vsum(const double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double e[3];
     ld_eps(b + d[3], e);
@@ -98,14 +103,14 @@ struct BGTasks {
     return acc;
   }
   template <int K>
-  static __device__ __forceinline__ void in_node(double* b, uint4 raw) {
+  static __device__ __forceinline__ void in_node(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
     st_aos(b, d[1], prop_col(m, vsum<K, false>(b, raw)));
   }
   template <int K>
-  static __device__ __forceinline__ void out_node(double* b, uint4 raw) {
+  static __device__ __forceinline__ void out_node(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
@@ -113,14 +118,14 @@ struct BGTasks {
   }
   // leaf descriptor field out = lb * 1024 + h: helicity h of the lb-th subset of the batch
   template <int K>
-  static __device__ __forceinline__ void in_leaf(double* b, uint4 raw) {
+  static __device__ __forceinline__ void in_leaf(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
     st_leaf<T::NHI>(b + (d[1] >> 10) * T::LEAFB, T::PHI, d[1] & 1023, prop_col(m, vsum<K, false>(b, raw)));
   }
   template <int K>
-  static __device__ __forceinline__ void out_leaf(double* b, uint4 raw) {
+  static __device__ __forceinline__ void out_leaf(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     st_leaf<T::NHO>(b + (d[1] >> 10) * T::LEAFB, T::UBL, d[1] & 1023, vsum<K, true>(b, raw));
   }
@@ -138,7 +143,7 @@ struct TaskFn {  // KIND: 0 vs_col, 1 vs_row, 2 phi, 3 ub
 };
 template <class T, int K, int KIND>
 struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
-  __device__ __forceinline__ void operator()(double* b, uint4 d) const {
+  __device__ __forceinline__ void operator()(double* b, const Desc<T::DW>& d) const {
     if (KIND == 0) BGTasks<T>::template in_node<K>(b, d);
     else if (KIND == 1) BGTasks<T>::template out_node<K>(b, d);
     else if (KIND == 2) BGTasks<T>::template in_leaf<K>(b, d);
@@ -148,14 +153,15 @@ struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
 
 // OFF: lane offset, so that two task kinds of one stage occupy different lanes / warps
 template <class T, int COUNT, class F, int OFF = 0>
-__device__ __forceinline__ void run_tasks8(double* base, int g, const uint4* __restrict__ tbl, F f) {
+__device__ __forceinline__ void run_tasks8(double* base, int g, const Desc<T::DW>* __restrict__ tbl, F f) {
   constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
   const int gl = (g + T::G - OFF) % T::G;
-  uint4 d[TRIPS];
+  Desc<T::DW> d[TRIPS];
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k) {
     const int t = gl + k * T::G;
-    d[k] = (t < COUNT) ? tbl[t] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int w = 0; w < T::DW / 8; ++w) d[k].v[w] = (t < COUNT) ? tbl[t].v[w] : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k)
@@ -331,7 +337,9 @@ __device__ __forceinline__ double group_msq(const double (&amp)[8], int g, int p
   if constexpr (T::G > 32) {
     if ((g & 31) == 0) base[T::RED + (g >> 5)] = sum;
     group_sync<T>(pb);
-    sum = base[T::RED] + base[T::RED + 1];
+    sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < T::G / 32; ++w) sum += base[T::RED + w];
   }
   return a.norm * sum;
 }

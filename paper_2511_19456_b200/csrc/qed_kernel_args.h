@@ -10,7 +10,7 @@ struct QedEvalArgs {
   long long n_points;
   int n_in_ph;                // photons 0..n_in_ph-1 are incoming (q = +k), the rest outgoing (q = -k)
   int e_out_particle;         // particle index of the outgoing electron
-  unsigned photon_particle;   // 4 bits per photon i: particle index of photon i
+  unsigned long long photon_particle;  // 4 bits per photon i: particle index of photon i
   unsigned long long ext_bit; // 4 bits per internal configuration bit: external particle index
   unsigned fixed_mask;        // internal configuration bits fixed by the process spec
   unsigned fixed_val;

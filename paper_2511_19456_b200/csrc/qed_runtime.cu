@@ -57,6 +57,18 @@ const void* qedbg_kernel_N6(int, int);
 const void* qedbg_mc_kernel_N6(int);
 int qedbg_num_variants_N6(void);
 void qedbg_config_N6(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N7(int, int);
+const void* qedbg_mc_kernel_N7(int);
+int qedbg_num_variants_N7(void);
+void qedbg_config_N7(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N8(int, int);
+const void* qedbg_mc_kernel_N8(int);
+int qedbg_num_variants_N8(void);
+void qedbg_config_N8(int, int*, int*, long long*, long long*);
+const void* qedbg_kernel_N9(int, int);
+const void* qedbg_mc_kernel_N9(int);
+int qedbg_num_variants_N9(void);
+void qedbg_config_N9(int, int*, int*, long long*, long long*);
 const void* qedregs_kernel_N2(int, int);
 int qedregs_num_variants_N2(void);
 const void* qedregs_kernel_N3(int, int);
@@ -100,6 +112,9 @@ const KernelEntry kBGKernels[] = {
     {qedbg_kernel_N4, qedbg_mc_kernel_N4, qedbg_config_N4, qedbg_num_variants_N4},
     {qedbg_kernel_N5, qedbg_mc_kernel_N5, qedbg_config_N5, qedbg_num_variants_N5},
     {qedbg_kernel_N6, qedbg_mc_kernel_N6, qedbg_config_N6, qedbg_num_variants_N6},
+    {qedbg_kernel_N7, qedbg_mc_kernel_N7, qedbg_config_N7, qedbg_num_variants_N7},
+    {qedbg_kernel_N8, qedbg_mc_kernel_N8, qedbg_config_N8, qedbg_num_variants_N8},
+    {qedbg_kernel_N9, qedbg_mc_kernel_N9, qedbg_config_N9, qedbg_num_variants_N9},
 };
 
 // launch variant from QED_VARIANT (tuning experiments); 0 = default, out-of-range -> 0
@@ -159,8 +174,15 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   const int N = in->n_photons + out->n_photons;
   if (N != n_photons + 1)
     return fail(QED_ERR_INVALID_ARGUMENT, "in.n_photons + out.n_photons must equal n_photons + 1");
-  if (n_photons < 1 || n_photons > 5)
-    return fail(QED_ERR_UNSUPPORTED, "supported photon counts: 1 <= n <= 5 (N = n+1 photons on the line)");
+  const int algorithm = options ? options->algorithm : QED_ALGO_CDAG;
+  if (algorithm != QED_ALGO_CDAG && algorithm != QED_ALGO_BERENDS_GIELE)
+    return fail(QED_ERR_INVALID_ARGUMENT, "unknown algorithm");
+  const int n_max = algorithm == QED_ALGO_BERENDS_GIELE ? 8 : 5;
+  if (n_photons < 1 || n_photons > n_max)
+    return fail(QED_ERR_UNSUPPORTED, algorithm == QED_ALGO_BERENDS_GIELE
+                                         ? "supported photon counts with QED_ALGO_BERENDS_GIELE: 1 <= n <= 8"
+                                         : "supported photon counts with QED_ALGO_CDAG: 1 <= n <= 5 (n = 6..8: use "
+                                           "QED_ALGO_BERENDS_GIELE)");
 
   qed_process* P = new (std::nothrow) qed_process;
   if (!P) return fail(QED_ERR_OUT_OF_MEMORY, "host allocation failed");
@@ -182,9 +204,9 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   a.n_in_ph = P->n_in_ph;
   a.e_out_particle = e_out;
   a.photon_particle = 0;
-  for (int i = 0; i < N; ++i) a.photon_particle |= (unsigned)photon_particle(i) << (4 * i);
+  for (int i = 0; i < N; ++i) a.photon_particle |= (unsigned long long)photon_particle(i) << (4 * i);
   // internal configuration bits: 0 = e-_in spin, 1 + i = photon i, N + 1 = e-_out spin
-  int ext_of_bit[10];
+  int ext_of_bit[12];
   ext_of_bit[0] = 0;
   for (int i = 0; i < N; ++i) ext_of_bit[1 + i] = photon_particle(i);
   ext_of_bit[N + 1] = e_out;
@@ -206,11 +228,6 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
     if (spin_of(j) < 0) norm *= 0.5;
   a.norm = norm;
 
-  const int algorithm = options ? options->algorithm : QED_ALGO_CDAG;
-  if (algorithm != QED_ALGO_CDAG && algorithm != QED_ALGO_BERENDS_GIELE) {
-    delete P;
-    return fail(QED_ERR_INVALID_ARGUMENT, "unknown algorithm");
-  }
   P->algorithm = algorithm;
   const KernelEntry& ke = algorithm == QED_ALGO_BERENDS_GIELE ? kBGKernels[N - 2] : kKernels[N - 2];
   // n = 1, 2: register-resident straight-line kernels (qed_eval_regs.cuh); n >= 3: lane-group
@@ -373,7 +390,7 @@ qed_status qed_get_process_info(const qed_process* P, qed_process_info* info) {
   if (!P || !info) return fail(QED_ERR_INVALID_ARGUMENT, "NULL argument");
   info->n_photons = P->n;
   info->n_ext = P->n_ext;
-  info->n_configs = 1 << P->n_ext;
+  info->n_configs = 1 << P->n_ext;   // up to 2^11
   long long f = 1;
   for (int i = 2; i <= P->N; ++i) f *= i;
   info->n_diagrams = (int)f;

@@ -23,7 +23,7 @@ def choose_launch(plan: Plan) -> tuple[int, int]:
     """(warps per block, resident blocks per SM) maximising resident warps under the
     shared-memory limit, keeping >= MIN_REGS registers per thread."""
     best = (0, 1, 1)
-    for wpb in (1, 2, 4, 8):
+    for wpb in (1, 2, 4, 8, 16):
         if wpb * 32 < plan.G or (wpb * 32) % plan.G:
             continue
         pb = wpb * 32 // plan.G
@@ -32,6 +32,8 @@ def choose_launch(plan: Plan) -> tuple[int, int]:
             break
         blocks = min(32, SMEM_PER_SM // (blk + SMEM_RESERVED_PER_BLOCK), 64 // wpb)
         blocks = min(blocks, 65536 // (MIN_REGS * wpb * 32))
+        if blocks < 1:
+            continue
         if blocks * wpb > best[0]:
             best = (blocks * wpb, wpb, blocks)
     return best[1], best[2]

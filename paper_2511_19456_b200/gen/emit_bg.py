@@ -13,19 +13,20 @@ from .emit import choose_launch, lane_offset
 from .lower_bg import BGPlan, make_bg_plan
 
 
-def _tbl(name, tasks):
+def _tbl(name, tasks, dw):
     rows = []
     for d in tasks:
-        assert len(d) <= 8 and max(d) < 65536
-        rows.append(list(d) + [0] * (8 - len(d)))
+        assert len(d) <= dw and max(d) < 65536
+        rows.append(list(d) + [0] * (dw - len(d)))
     if not rows:
-        return f"__device__ const uint4 {name}[1] = {{}};\n"
+        return f"__device__ const qed::Desc<{dw}> {name}[1] = {{}};\n"
     packed = []
     for r in rows:
-        w = [r[i] | (r[i + 1] << 16) for i in range(0, 8, 2)]
-        packed.append("{" + ", ".join(f"0x{x:08x}u" for x in w) + "}")
-    body = ",\n  ".join(", ".join(packed[i:i + 4]) for i in range(0, len(packed), 4))
-    return f"__device__ const uint4 {name}[{len(rows)}] = {{\n  {body}}};\n"
+        w = [r[i] | (r[i + 1] << 16) for i in range(0, dw, 2)]
+        quads = ["{" + ", ".join(f"0x{x:08x}u" for x in w[q:q + 4]) + "}" for q in range(0, len(w), 4)]
+        packed.append("{{" + ", ".join(quads) + "}}")
+    body = ",\n  ".join(", ".join(packed[i:i + 2]) for i in range(0, len(packed), 2))
+    return f"__device__ const qed::Desc<{dw}> {name}[{len(rows)}] = {{\n  {body}}};\n"
 
 
 def emit_bg_source(plan: BGPlan) -> str:
@@ -50,18 +51,36 @@ def emit_bg_source(plan: BGPlan) -> str:
     interiors = "\n".join(lines) if lines else "    (void)base; (void)g; (void)pb;"
     B = plan.setb
     n_in, n_out = B * len(plan.set_in[0]), B * len(plan.set_out[0])
+    stage_struct = [[(kind, K, len(t)) for kind, K, t in st] for st in plan.set_stages[0]]
+    n_rec = sum(c for st in stage_struct for _, _, c in st)
     set_flat = []
-    for s0 in range(0, len(plan.sets), B):       # one batch: all in-leaves, then all out-leaves
+    for s0 in range(0, len(plan.sets), B):       # one batch: recomputed levels, all in-leaves, all out-leaves
+        assert B == 1 or n_rec == 0
+        for st in plan.set_stages[s0]:
+            for _, _, t in st:
+                set_flat += t
         for q in range(B):
             set_flat += plan.set_in[s0 + q]
         for q in range(B):
             set_flat += plan.set_out[s0 + q]
-    per_set = n_in + n_out
+    per_set = n_rec + n_in + n_out
+    rec_lines, off = [], 0
+    for st in stage_struct:
+        prev = 0
+        for q, (kind, K, cnt) in enumerate(st):
+            lo = lane_offset(prev, plan.G) if q > 0 else 0
+            kid = 0 if kind == "in" else 1
+            rec_lines.append(f"    qed::run_tasks8<T, {cnt}, qed::BGFn<T, {K}, {kid}>, {lo}>(base, g, "
+                             f"k_sets + (si / {B}) * {per_set} + {off}, qed::BGFn<T, {K}, {kid}>{{}});")
+            off += cnt
+            prev = cnt
+        rec_lines.append("    qed::group_sync<T>(pb);")
+    rec_code = "\n".join(rec_lines) + ("\n" if rec_lines else "")
     lo = lane_offset(n_in, plan.G)
-    run_set = (f"    qed::run_tasks8<T, {n_in}, qed::BGFn<T, {plan.j}, 2>, 0>(base, g, k_sets + (si / {B}) * {per_set}, "
+    run_set = rec_code + (f"    qed::run_tasks8<T, {n_in}, qed::BGFn<T, {plan.j}, 2>, 0>(base, g, k_sets + (si / {B}) * {per_set} + {n_rec}, "
                f"qed::BGFn<T, {plan.j}, 2>{{}});\n"
                f"    qed::run_tasks8<T, {n_out}, qed::BGFn<T, {N - plan.j}, 3>, {lo}>(base, g, "
-               f"k_sets + (si / {B}) * {per_set} + {n_in}, qed::BGFn<T, {N - plan.j}, 3>{{}});")
+               f"k_sets + (si / {B}) * {per_set} + {n_rec + n_in}, qed::BGFn<T, {N - plan.j}, 3>{{}});")
     set_pos = [p for ps in plan.set_pos for p in ps]
     set_mask = [sum(1 << x for x in A) for A in plan.sets]
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in plan.flops.items())
@@ -77,7 +96,8 @@ def emit_bg_source(plan: BGPlan) -> str:
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_bg.py -- do not edit.
 // Berends-Giele (distributive rewrite of the node-reduced CDAG, NEXT #1) for N = {N} photons (n = {N - 1}):
 // {len(plan.sets)} photon subsets A (|A| = j = {plan.j}), one join each, {plan.H} configurations,
-// G = {plan.G} lanes per point, {B} subsets per leaf stage, {plan.stride * 8} B shared memory per point;
+// G = {plan.G} lanes per point, {B} subsets per leaf stage, {plan.stride * 8} B shared memory per point,
+// current levels <= {plan.store} stored (deeper ones recomputed per subset: +{plan.recompute_flops} executed flops);
 // variants {vs}.
 // Algorithmic FP64 flops per point:
 {flops_comment}
@@ -86,12 +106,12 @@ def emit_bg_source(plan: BGPlan) -> str:
 
 namespace {ns} {{
 
-{_tbl("k_levels", lev_flat)}{_tbl("k_sets", set_flat)}
+{_tbl("k_levels", lev_flat, plan.dw)}{_tbl("k_sets", set_flat, plan.dw)}
 __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str, set_pos))}}};
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
 
 struct T {{
-  static constexpr int N = {N}, J = {plan.j}, G = {plan.G};
+  static constexpr int N = {N}, J = {plan.j}, G = {plan.G}, DW = {plan.dw};
   static constexpr int STRIDE = {plan.stride};
   static constexpr int {lay};
   static constexpr int NSIG = 1, NTAU = 1, NHI = {plan.n_hi}, NHO = {plan.n_ho};
@@ -134,7 +154,7 @@ void qedbg_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, 
 """
 
 
-def generate_bg(out_dir: str, Ns=(2, 3, 4, 5, 6)) -> list[str]:
+def generate_bg(out_dir: str, Ns=(2, 3, 4, 5, 6, 7, 8, 9)) -> list[str]:
     os.makedirs(out_dir, exist_ok=True)
     paths = []
     for N in Ns:

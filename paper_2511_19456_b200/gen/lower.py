@@ -139,7 +139,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
         off += size
 
     alloc("MOM", 4 * (N + 2))
-    alloc("RED", 2)                  # cross-warp reduction scratch (64-lane groups)
+    alloc("RED", max(2, G // 32))    # cross-warp reduction scratch (groups of > 32 lanes)
     alloc("EPS", N * 2 * 4)          # [photon][lam][e1, e2, e3, pad]
     alloc("MASK", (1 << N) * 6)      # [subset][Qp, Qm, qx, qy, qz, pad]
     alloc("U", 2 * 8, 8)             # [s] spinor (AoS, swizzled)

@@ -79,14 +79,26 @@ def default_setb(N: int, j: int) -> int:
     return b
 
 
-def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPlan:
+def default_bg_store(N: int, j: int) -> int:
+    """Current levels stored per point; deeper interior levels are recomputed per subset when storing
+    them would push shared memory past ~110 KB per point (n >= 7)."""
+    def spinors(store):
+        return sum(math.comb(N, k) << (k + 1) for k in range(1, min(j, store + 1))) + \
+            sum(math.comb(N, k) << (k + 1) for k in range(1, min(N - j, store + 1)))
+    return N if spinors(N) * 64 <= 110 * 1024 else 2
+
+
+def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
     G = 1 << N
     full = (1 << N) - 1
+    if store is None:
+        store = default_bg_store(N, j)
+    recompute = store + 1 < max(j, N - j)
     if setb is None:
-        setb = default_setb(N, j)
+        setb = 1 if recompute else default_setb(N, j)
     lay: dict[str, int] = {}
     off = 0
 
@@ -97,21 +109,27 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPla
         off += size
 
     alloc("MOM", 4 * (N + 2))
-    alloc("RED", 2)
+    alloc("RED", max(2, G // 32))
     alloc("EPS", N * 2 * 4)
     alloc("MASK", (1 << N) * 6)
     alloc("U", 16, 8)
     alloc("UB", 16, 8)
     in_idx: dict[int, dict[tuple, int]] = {}
     out_idx: dict[int, dict[tuple, int]] = {}
-    for k in range(1, j):
+    for k in range(1, min(j, store + 1)):
         subs = _subsets(N, k)
         alloc(f"IN{k}", len(subs) * (1 << (k + 1)) * 8, 8)
         in_idx[k] = {s: i for i, s in enumerate(subs)}
-    for k in range(1, N - j):
+    for k in range(1, min(N - j, store + 1)):
         subs = _subsets(N, k)
         alloc(f"OUT{k}", len(subs) * (1 << (k + 1)) * 8, 8)
         out_idx[k] = {s: i for i, s in enumerate(subs)}
+    # per-subset recomputed levels: subsets of size k inside A (|A| = j) / inside A^c (|A^c| = N - j)
+    for k in range(store + 1, j):
+        alloc(f"SIN{k}", math.comb(j, k) * (1 << (k + 1)) * 8, 8)
+    for k in range(store + 1, N - j):
+        alloc(f"SOUT{k}", math.comb(N - j, k) * (1 << (k + 1)) * 8, 8)
+    set_local: dict[tuple, int] = {}
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
     leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL)
     alloc("PHI", 4 * n_hi * 2, 8)
@@ -140,6 +158,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPla
         k = len(S)
         if k == 0:
             return (lay["U"] if side == "in" else lay["UB"]) + h * 8
+        if k > store:
+            idx = set_local[(side, S)]
+            return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + (idx * (1 << (k + 1)) + h) * 8
         idx = (in_idx if side == "in" else out_idx)[k][S]
         return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (idx * (1 << (k + 1)) + h) * 8
 
@@ -155,7 +176,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPla
 
     plan = BGPlan(N=N, j=j, G=G, sets=[], layout=lay, stride=stride)
     plan.setb = setb
-    for k in range(1, max(j, N - j)):
+    plan.store = store
+    plan.set_stages = []
+    for k in range(1, min(max(j, N - j), store + 1)):
         if k < j:
             t = [task("in", S, h, node_off("in", S, h), mask_off(msk(S)))
                  for S in _subsets(N, k) for h in range(1 << (k + 1))]
@@ -173,6 +196,25 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPla
         for k, x in enumerate(Ac):
             pos[x] = 1 + k
         plan.set_pos.append(pos)
+        # recomputed interior levels of this subset (stored levels are shared by all subsets)
+        stages = []
+        set_local.clear()
+        for k in range(store + 1, max(j, N - j)):
+            st = []
+            if k < j:
+                subs = list(itertools.combinations(A, k))
+                for i, S in enumerate(subs):
+                    set_local[("in", S)] = i
+                st.append(("in", k, [task("in", S, h, node_off("in", S, h), mask_off(msk(S)))
+                                     for S in subs for h in range(1 << (k + 1))]))
+            if k < N - j:
+                subs = list(itertools.combinations(Ac, k))
+                for i, T in enumerate(subs):
+                    set_local[("out", T)] = i
+                st.append(("out", k, [task("out", T, h, node_off("out", T, h), mask_off(full & ~msk(T)))
+                                      for T in subs for h in range(1 << (k + 1))]))
+            stages.append(st)
+        plan.set_stages.append(stages)
         lb = (len(plan.sets) - 1) % setb          # leaf buffer of this subset within its batch
         plan.set_in.append([task("in", A, h, lb * 1024 + h, mask_off(msk(A))) for h in range(n_hi)])
         plan.set_out.append([task("out", Ac, h, lb * 1024 + h, 0) for h in range(n_ho)])
@@ -186,6 +228,13 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None) -> BGPla
     n_in = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(1, j + 1))
     n_out = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(1, N - j)) + \
         math.comb(N, N - j) * (1 << (N - j + 1)) * vflops(N - j)
+    plan.max_k = max(j, N - j)
+    plan.dw = 8 if plan.max_k <= 3 else 16          # descriptor width in ushort
+    rec = sum(len(t) * (vflops(k) + F["S"]) for stages in plan.set_stages for st in stages for _, k, t in st)
+    stored_rec = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"])
+                     for k in range(store + 1, j)) + \
+        sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(store + 1, N - j))
+    plan.recompute_flops = rec - stored_rec          # executed on top of the algorithmic count
     plan.flops = {
         "external": N * F["EPS"] + 2 * F["SPINOR"],
         "propagator_constants": ((1 << N) - 2) * F["MASK"],

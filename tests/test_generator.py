@@ -134,3 +134,24 @@ def test_bg_flop_counts():
     assert got == [2260, 7792, 27100, 90792, 310324]
     cdag = [make_plan(n + 1).flops_per_point for n in range(1, 6)]
     assert cdag[4] / got[4] > 19
+
+
+@pytest.mark.parametrize("N,store", [(5, 1), (6, 1), (7, None)])
+def test_bg_recompute_and_large_tables_match_oracle(N, store):
+    """Per-subset recomputation of deep current levels (n >= 7 default) and the n = 6 tables."""
+    from paper_2511_19456_b200.gen.interp import eval_point_bg
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    n = N - 1
+    plan = make_bg_plan(N, store=store)
+    mom = synthetic.rambo_cm(n, 1, sqrt_s=5.0, seed=600 + n).numpy()
+    A = oracle.amps(1, n, mom)
+    B = eval_point_bg(plan, mom[0], 1)
+    assert np.max(np.abs(A[0] - B)) <= 1e-12 * np.max(np.abs(A[0]))
+
+
+def test_bg_default_plans_n7_n8():
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    p8 = make_bg_plan(8)
+    assert p8.store == 2 and p8.dw == 16 and p8.stride * 8 < 64 * 1024
+    p9 = make_bg_plan(9)
+    assert p9.store == 2 and p9.stride * 8 < 100 * 1024

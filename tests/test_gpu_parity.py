@@ -281,3 +281,45 @@ def test_photons_along_the_beam_axis(qed, algorithm):
     got = _gpu_msq(qed, qed.Process(2, algorithm=algorithm), torch.from_numpy(base))
     ref = oracle.msq(1, 2, base)
     assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+# ---------------------------------------------------------------- n = 6..8 (NEXT #2, Berends-Giele only)
+
+def test_bg_n6_matches_oracle(qed):
+    n = 6
+    mom = synthetic.rambo_cm(n, 16, sqrt_s=5.0, seed=1106)
+    got = _gpu_msq(qed, qed.Process(n, algorithm="bg"), mom)
+    ref = oracle.msq(1, n, mom.numpy())
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+@pytest.mark.parametrize("n", [7, 8])
+def test_bg_large_n_matches_golden_oracle(qed, n):
+    """Oracle values precomputed by tools/make_golden.py (oracle only; ~100 s / 30 min per point)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_n{n}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    mom = torch.tensor(g["momenta"], dtype=torch.float64)
+    got = _gpu_msq(qed, qed.Process(n, algorithm="bg"), mom)
+    ref = np.array(g["msq"])
+    assert np.max(np.abs(got / ref - 1)) <= TOL
+
+
+@pytest.mark.parametrize("n", [6, 7, 8])
+def test_bg_large_n_invariances(qed, n):
+    """Properties that hold at any size: Lorentz invariance of the spin/polarisation-summed |M|^2 and
+    Bose symmetry under a permutation of the outgoing photons."""
+    mom = synthetic.rambo_cm(n, 1024, sqrt_s=5.0, seed=1200 + n)
+    proc = qed.Process(n, algorithm="bg")
+    a = _gpu_msq(qed, proc, mom)
+    b = _gpu_msq(qed, proc, synthetic.boost_rotate(mom, seed=3, max_rapidity=1.0))
+    perm = torch.roll(torch.arange(n), 1)
+    mom2 = mom.clone()
+    mom2[:, 3:] = mom[:, 3 + perm]
+    c = _gpu_msq(qed, proc, mom2)
+    assert np.all(np.isfinite(a)) and np.all(a > 0)
+    assert np.max(np.abs(b / a - 1)) <= 1e-9
+    assert np.max(np.abs(c / a - 1)) <= 1e-12

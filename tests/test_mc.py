@@ -182,3 +182,21 @@ def test_gpu_mc_cross_section_klein_nishina():
                                      - (1 + 3 * x) / (1 + 2 * x) ** 2)
     assert abs(res["sigma"] - kn) < 5 * res["error"]
     assert res["error"] < 1e-3 * kn
+
+
+@pytest.mark.gpu
+def test_gpu_mc_sum_bg_n6_matches_oracle():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_19456_b200 import qed
+    n, first, count = 6, 8190, 24
+    proc = qed.Process(n, algorithm="bg")
+    nch = mc.n_chunks(first + count)
+    partials = torch.zeros(3 * nch, dtype=torch.float64, device="cuda")
+    proc.mc_sum(partials, 5.0, 0.25, 99, first, count)
+    torch.cuda.synchronize()
+    got = partials.cpu().numpy().reshape(nch, 3)
+    ref = oracle.mc_sum(n, 5.0, 0.25, 99, first, count)
+    assert np.array_equal(got[:, 2], ref[:, 2])
+    nz = ref[:, 0] > 0
+    assert np.all(np.abs(got[nz, :2] / ref[nz, :2] - 1) <= 1e-10)

@@ -1,0 +1,33 @@
+"""Small invocation of every kernel family through the C ABI, for compute-sanitizer
+(tools/sanitize.sh runs it under memcheck, racecheck, synccheck and initcheck on one GPU).
+Sizes are small but ragged so that every code path (tails, multiple groups per warp, two-warp
+groups, per-configuration output, MC chunks) is exercised."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synthetic  # noqa: E402
+from paper_2511_19456_b200 import mc, qed  # noqa: E402
+
+torch.cuda.set_device(0)
+cases = [("cdag", n, 37) for n in (1, 2, 3, 4, 5)] + [("bg", n, 19) for n in (1, 2, 3, 4, 5, 6, 7)]
+if len(sys.argv) > 1 and sys.argv[1] == "quick":
+    cases = [("cdag", 2, 37), ("cdag", 3, 21), ("cdag", 5, 3), ("bg", 5, 3), ("bg", 7, 2)]
+for algo, n, npts in cases:
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=5 + n)
+    soa = synthetic.to_soa(mom).cuda()
+    proc = qed.Process(n, algorithm=algo)
+    out = torch.empty(npts, dtype=torch.float64, device="cuda")
+    proc.eval_msq(soa, out)
+    cfg = torch.empty(npts << (n + 3), dtype=torch.float64, device="cuda")
+    proc.eval_msq_configs(soa, cfg, npts)
+    if n <= 5:
+        part = torch.zeros(3 * mc.n_chunks(mc.CHUNK + npts), dtype=torch.float64, device="cuda")
+        proc.mc_sum(part, 5.0, 0.25, 3, mc.CHUNK - 5, npts)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all(), (algo, n)
+    print(algo, n, "ok", flush=True)
