@@ -322,4 +322,4 @@ def test_bg_large_n_invariances(qed, n):
     c = _gpu_msq(qed, proc, mom2)
     assert np.all(np.isfinite(a)) and np.all(a > 0)
     assert np.max(np.abs(b / a - 1)) <= 1e-9
-    assert np.max(np.abs(c / a - 1)) <= 1e-12
+    assert np.max(np.abs(c / a - 1)) <= TOL      # rounding order changes with the permutation
