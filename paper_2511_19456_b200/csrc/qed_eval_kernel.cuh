@@ -249,7 +249,7 @@ __device__ __forceinline__ void join_set(const double* __restrict__ base, int hi
       p0[c] = ld2(prow + c * T::NHI * 2 + h0);
       p1[c] = ld2(prow + c * T::NHI * 2 + h1);
     }
-#pragma unroll 1
+#pragma unroll(T::NTAU >= 4 ? 2 : 1)   // two tau per iteration: next tau's leaf loads overlap this tau's MACs
     for (int tu = 0; tu < T::NTAU; ++tu) {
       const double* urow = base + T::UBL + tu * 4 * T::NHO * 2;
       c2 u0[4], u1[4];

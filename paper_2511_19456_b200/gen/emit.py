@@ -70,12 +70,9 @@ def _tasks(name, tasks):
 KIND_FN = {"vs_col": "vs_col", "vs_row": "vs_row", "phi": "phi", "ub": "ub"}
 
 
-def emit_source(plan: Plan) -> str:
+def emit_plan_namespace(plan: Plan, ns: str) -> str:
+    """Task tables + traits struct T of one lowered plan, in namespace `ns`."""
     N, L = plan.N, plan.layout
-    ns = f"qedgen_N{N}"
-    wpb, min_blocks = choose_launch(plan)
-    vs = variants(plan)
-    # stored interior levels
     in_flat, out_flat, lines = [], [], []
     for lv in range(max(len(plan.in_levels), len(plan.out_levels))):
         if lv < len(plan.in_levels):
@@ -90,7 +87,6 @@ def emit_source(plan: Plan) -> str:
             out_flat += t
         lines.append("    qed::group_sync<T>(pb);")
     interiors = "\n".join(lines) if lines else "    (void)base; (void)g; (void)pb;"
-    # per-set stages: identical structure for every set; flatten set-major
     struct = [[(k, len(t)) for k, t in st] for st in plan.set_stages[0]]
     per_set = sum(c for st in struct for _, c in st)
     set_flat = []
@@ -117,35 +113,14 @@ def emit_source(plan: Plan) -> str:
     for tbl in (in_flat, out_flat, set_flat):
         for t in tbl:
             assert max(t) < 65536
-    fl = plan.flops
-    flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     lay = ", ".join(f"{k} = {L[k]}" for k in ("MOM", "RED", "EPS", "MASK", "U", "UB", "PHI", "UBL"))
-    variant_structs = "".join(
-        f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }};\n"
-        for i, (w, m, a, p) in enumerate(vs))
-    kernel_cases = "\n".join(
-        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{i}, true>\n"
-        f"                                      : (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{i}, false>;"
-        for i in range(len(vs)))
-    mc_cases = "\n".join(
-        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{ns}::T, {ns}::V{i}>;"
-        for i in range(len(vs)))
-    src = f"""// GENERATED by paper_2511_19456_b200/gen/emit.py -- do not edit.
-// Process size N = {N} photons (n = {N - 1}): {len(plan.sets)} photon subsets A (|A| = j = {plan.j}),
-// {plan.n_sigma} x {plan.n_tau} diagrams per subset, {plan.H} spin/polarisation configurations,
-// G = {plan.G} lanes per point; launch variants (warps/block, min blocks/SM, acc split, prefetch): {vs},
-// {plan.stride * 8} B shared memory per point, interior levels <= {plan.store} stored per point.
-// Algorithmic FP64 flops per point (node-reduced, helicity-shared DAG):
-{flops_comment}
-//   {'total':22s} {plan.flops_per_point:>10d}   (executed {sum(plan.executed_flops.values())})
-#include "../qed_mc_kernel.cuh"
-
-namespace {ns} {{
+    return f"""namespace {ns} {{
 
 {_tasks("k_in_tasks", in_flat)}{_tasks("k_out_tasks", out_flat)}{_tasks("k_set_tasks", set_flat)}
 __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str, set_pos))}}};
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
 
+// interior levels <= {plan.store} stored per point, {plan.stride * 8} B shared memory per point
 struct T {{
   static constexpr int N = {N}, J = {plan.j}, G = {plan.G};
   static constexpr int STRIDE = {plan.stride};
@@ -162,9 +137,54 @@ struct T {{
 {run_set}
   }}
 }};
-{variant_structs}
-}}  // namespace {ns}
 
+}}  // namespace {ns}
+"""
+
+
+def plan_variants(N: int) -> list[Plan]:
+    """Lowered plans compiled for one process size: the default, plus (n = 4) one that recomputes the
+    second out-side trie level per subset (22 KB -> 15 KB of shared memory per point)."""
+    plans = [make_plan(N)]
+    if N == 5:
+        plans.append(make_plan(N, store=1))
+    return plans
+
+
+def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
+    N = plan.N
+    plans = [plan] + list(extra or [])
+    nss = [f"qedgen_N{N}"] + [f"qedgen_N{N}_p{i}" for i in range(1, len(plans))]
+    vs = []   # (plan index, wpb, min blocks, AS, PF)
+    for pi, p in enumerate(plans):
+        vs += [(pi,) + v for v in variants(p)]
+    fl = plan.flops
+    flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
+    bodies = "\n".join(emit_plan_namespace(p, ns) for p, ns in zip(plans, nss))
+    variant_structs = "".join(
+        f"namespace {nss[pi]} {{ struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }}; }}\n"
+        for i, (pi, w, m, a, p) in enumerate(vs))
+    kernel_cases = "\n".join(
+        f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, true>\n"
+        f"                                      : (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, false>;"
+        for i, (pi, *_) in enumerate(vs))
+    mc_cases = "\n".join(
+        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{nss[pi]}::T, {nss[pi]}::V{i}>;"
+        for i, (pi, *_) in enumerate(vs))
+    strides = ", ".join(str(plans[pi].stride) for pi, *_ in vs)
+    flops = ", ".join(f"{plans[pi].flops_per_point}LL" for pi, *_ in vs)
+    return f"""// GENERATED by paper_2511_19456_b200/gen/emit.py -- do not edit.
+// Process size N = {N} photons (n = {N - 1}): {len(plan.sets)} photon subsets A (|A| = j = {plan.j}),
+// {plan.n_sigma} x {plan.n_tau} diagrams per subset, {plan.H} spin/polarisation configurations,
+// G = {plan.G} lanes per point; launch variants (plan, warps/block, min blocks/SM, acc split, prefetch):
+// {vs}
+// Algorithmic FP64 flops per point (node-reduced, helicity-shared DAG):
+{flops_comment}
+//   {'total':22s} {plan.flops_per_point:>10d}   (executed {sum(plan.executed_flops.values())})
+#include "../qed_mc_kernel.cuh"
+
+{bodies}
+{variant_structs}
 extern "C" {{
 int qedgen_num_variants_N{N}(void) {{ return {len(vs)}; }}
 const void* qedgen_kernel_N{N}(int per_config, int variant) {{
@@ -179,25 +199,26 @@ const void* qedgen_mc_kernel_N{N}(int variant) {{
 }}
 void qedgen_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, long long* smem_per_block,
                         long long* flops_per_point) {{
-  static const int wpb[{len(vs)}] = {{{", ".join(str(v[0]) for v in vs)}}};
+  static const int wpb[{len(vs)}] = {{{", ".join(str(v[1]) for v in vs)}}};
+  static const int stride[{len(vs)}] = {{{strides}}};
+  static const long long flops[{len(vs)}] = {{{flops}}};
   const int w = wpb[variant];
   *warps_per_block = w;
-  *points_per_warp = 32 / {ns}::T::G;   // 0 when a point spans two warps
-  *smem_per_block = (long long)(w * 32 / {ns}::T::G) * {ns}::T::STRIDE * 8;
-  *flops_per_point = {ns}::T::FLOPS_PER_POINT;
+  *points_per_warp = 32 / {plan.G};   // 0 when a point spans several warps
+  *smem_per_block = (long long)(w * 32 / {plan.G}) * stride[variant] * 8;
+  *flops_per_point = flops[variant];  // algorithmic (identical for every plan of this size)
 }}
 }}
 """
-    return src
 
 
 def generate_all(out_dir: str, Ns=(2, 3, 4, 5, 6)) -> list[str]:
     os.makedirs(out_dir, exist_ok=True)
     paths = []
     for N in Ns:
-        plan = make_plan(N)
+        plans = plan_variants(N)
         path = os.path.join(out_dir, f"qed_eval_N{N}.cu")
-        src = emit_source(plan)
+        src = emit_source(plans[0], plans[1:])
         if not os.path.exists(path) or open(path).read() != src:
             with open(path, "w") as f:
                 f.write(src)

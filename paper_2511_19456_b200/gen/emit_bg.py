@@ -33,7 +33,9 @@ def emit_bg_source(plan: BGPlan) -> str:
     N, L = plan.N, plan.layout
     ns = f"qedbg_N{N}"
     wpb, mb = choose_launch(plan)
-    vs = [(wpb, max(1, min(mb, 65536 // (152 * wpb * 32))), 4, 1), (wpb, mb, 2, 1)]   # r06 sweep: AS = 4 first
+    mb4 = max(1, min(mb, 65536 // (152 * wpb * 32)))
+    # r06/r10 sweeps: AS = 4 first unless its register budget costs resident blocks (n >= 7)
+    vs = [(wpb, mb4, 4, 1), (wpb, mb, 2, 1)] if mb4 == mb else [(wpb, mb, 2, 1), (wpb, mb4, 4, 1)]
     lev_flat, lines = [], []
     prev_count, prev_k = 0, None
     for i, (kind, K, tasks) in enumerate(plan.levels):
