@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-per-n", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning sweeps)")
+    ap.add_argument("--no-mc", action="store_true", help="skip the MC cross-section leg (configs[3])")
     ap.add_argument("--algorithm", default="cdag", choices=["cdag", "bg"],
                     help="cdag: the paper's node-reduced diagram DAG (headline); bg: Berends-Giele rewrite")
     return ap.parse_args()
@@ -238,6 +239,37 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- our arm
+def run_mc(args, world, rank, stream, dev) -> dict:
+    """BASELINE.json configs[3]: e- gamma -> e- + 4 gamma, 2^24 points in total, Monte-Carlo cross-section:
+    each rank generates + evaluates its chunk-aligned share on its GPU (fused qed_mc_sum), then ONE
+    all_reduce of the chunk partial sums (NCCL on the GPU box).  Timed with CUDA events around the whole
+    step (kernel + all-reduce), max over ranks.  Both algorithms give the same sigma (same points)."""
+    import torch
+
+    from paper_2511_19456_b200 import mc, qed
+    out = {"n": 4, "points_total": 1 << 24, "sqrt_s": args.sqrt_s, "omega_min": 0.05 * args.sqrt_s}
+    for algo in ("bg", "cdag"):
+        proc = qed.Process(4, algorithm=algo)
+        N = out["points_total"]
+        res = {}
+
+        def step():
+            res.update(mc.mc_cross_section(proc, args.sqrt_s, 0.05 * args.sqrt_s, 4, N, device=dev, stream=stream))
+        step()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
+        out[algo] = {"value": N / t, "unit": UNIT, "ms": 1e3 * t, "sigma": res["sigma"], "error": res["error"],
+                     "n_pass": res["n_pass"]}
+    out["sigma_unit"] = "m_e^-2 (natural units)"
+    return out
+
+
 def sweep_per_n(args, world, stream, dev, algorithm: str) -> dict:
     """Every process size n = 1..5 at its own batch size, same timing protocol, 5 steps."""
     import torch
@@ -334,6 +366,8 @@ def run_b200(args, world, rank, local):
         per_n = sweep_per_n(args, world, stream, dev, "cdag")
         per_n_bg = sweep_per_n(args, world, stream, dev, "bg")
 
+    mc_res = None if args.no_mc else run_mc(args, world, rank, stream, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(n, 12.0, args.sqrt_s, args.seed)
@@ -355,7 +389,7 @@ def run_b200(args, world, rank, local):
                                                             "grid_blocks")}, variant=os.environ.get("QED_VARIANT", "0"))},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "fp64_dfma_microbench": peak, "per_n": per_n,
-            "per_n_berends_giele": per_n_bg,
+            "per_n_berends_giele": per_n_bg, "mc": mc_res,
         }
         print(json.dumps(line), flush=True)
 
