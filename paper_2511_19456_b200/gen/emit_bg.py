@@ -57,18 +57,20 @@ def emit_bg_source(plan: BGPlan) -> str:
     n_rec = sum(c for st in stage_struct for _, _, c in st)
     set_flat = []
     for s0 in range(0, len(plan.sets), B):       # one batch: recomputed levels, all in-leaves, all out-leaves
-        assert B == 1 or n_rec == 0
-        for st in plan.set_stages[s0]:
-            for _, _, t in st:
-                set_flat += t
+        for lvl in range(len(stage_struct)):      # level by level, every subset of the batch
+            for kk in range(len(stage_struct[lvl])):
+                for q in range(B):
+                    set_flat += plan.set_stages[s0 + q][lvl][kk][2]
         for q in range(B):
             set_flat += plan.set_in[s0 + q]
         for q in range(B):
             set_flat += plan.set_out[s0 + q]
+    n_rec *= B
     per_set = n_rec + n_in + n_out
     rec_lines, off = [], 0
     for st in stage_struct:
         prev = 0
+        st = [(kind, K, cnt * B) for kind, K, cnt in st]
         for q, (kind, K, cnt) in enumerate(st):
             lo = lane_offset(prev, plan.G) if q > 0 else 0
             kid = 0 if kind == "in" else 1

@@ -217,15 +217,16 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     H = plan.H
     amp = np.zeros(H, dtype=complex)
     for si, A in enumerate(plan.sets):
-        for stage in plan.set_stages[si]:
-            for kind, K, tasks in stage:
-                for d in tasks:
-                    if kind == "in":
-                        put_aos(d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
-                    else:
-                        put_aos(d[1], _prop_row(sm[d[0]: d[0] + 5], vsum(d, True)))
         lb = si % plan.setb
         if lb == 0:
+            for sj in range(si, si + plan.setb):
+                for stage in plan.set_stages[sj]:
+                    for kind, K, tasks in stage:
+                        for d in tasks:
+                            if kind == "in":
+                                put_aos(d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
+                            else:
+                                put_aos(d[1], _prop_row(sm[d[0]: d[0] + 5], vsum(d, True)))
             for sj in range(si, si + plan.setb):
                 for d in plan.set_in[sj]:
                     put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))

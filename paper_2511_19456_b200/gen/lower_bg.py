@@ -79,6 +79,16 @@ def default_setb(N: int, j: int) -> int:
     return b
 
 
+def default_setb_rec(N: int, j: int) -> int:
+    """Subsets per stage when deep levels are recomputed per subset: the largest power of two <= 4
+    that divides the number of subsets (each batched subset gets its own recompute / leaf slot)."""
+    n_sets = math.comb(N, j)
+    b = 4
+    while n_sets % b:
+        b //= 2
+    return b
+
+
 def default_bg_store(N: int, j: int) -> int:
     """Current levels stored per point; deeper interior levels are recomputed per subset when storing
     them would push shared memory past ~110 KB per point (n >= 7)."""
@@ -98,7 +108,7 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         store = default_bg_store(N, j)
     recompute = store + 1 < max(j, N - j)
     if setb is None:
-        setb = 1 if recompute else default_setb(N, j)
+        setb = default_setb(N, j) if not recompute else min(4, default_setb_rec(N, j))
     lay: dict[str, int] = {}
     off = 0
 
@@ -126,10 +136,11 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         out_idx[k] = {s: i for i, s in enumerate(subs)}
     # per-subset recomputed levels: subsets of size k inside A (|A| = j) / inside A^c (|A^c| = N - j)
     for k in range(store + 1, j):
-        alloc(f"SIN{k}", math.comb(j, k) * (1 << (k + 1)) * 8, 8)
+        alloc(f"SIN{k}", setb * math.comb(j, k) * (1 << (k + 1)) * 8, 8)
     for k in range(store + 1, N - j):
-        alloc(f"SOUT{k}", math.comb(N - j, k) * (1 << (k + 1)) * 8, 8)
+        alloc(f"SOUT{k}", setb * math.comb(N - j, k) * (1 << (k + 1)) * 8, 8)
     set_local: dict[tuple, int] = {}
+    cur_slot = [0]
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
     leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL)
     alloc("PHI", 4 * n_hi * 2, 8)
@@ -160,7 +171,8 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
             return (lay["U"] if side == "in" else lay["UB"]) + h * 8
         if k > store:
             idx = set_local[(side, S)]
-            return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + (idx * (1 << (k + 1)) + h) * 8
+            slot = cur_slot[0] * math.comb(j if side == "in" else N - j, k)   # this subset's batch slot
+            return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + ((slot + idx) * (1 << (k + 1)) + h) * 8
         idx = (in_idx if side == "in" else out_idx)[k][S]
         return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (idx * (1 << (k + 1)) + h) * 8
 
@@ -199,6 +211,7 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         # recomputed interior levels of this subset (stored levels are shared by all subsets)
         stages = []
         set_local.clear()
+        cur_slot[0] = (len(plan.sets) - 1) % setb
         for k in range(store + 1, max(j, N - j)):
             st = []
             if k < j:

@@ -150,8 +150,9 @@ def test_bg_recompute_and_large_tables_match_oracle(N, store):
 
 
 def test_bg_default_plans_n7_n8():
+    """n = 7, 8: levels above 2 recomputed per subset, two subsets per stage, fits one block's shared memory."""
     from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
-    p8 = make_bg_plan(8)
-    assert p8.store == 2 and p8.dw == 16 and p8.stride * 8 < 64 * 1024
-    p9 = make_bg_plan(9)
-    assert p9.store == 2 and p9.stride * 8 < 100 * 1024
+    for N in (8, 9):
+        p = make_bg_plan(N)
+        assert p.store == 2 and p.dw == 16 and p.setb == 2
+        assert p.stride * 8 < 227 * 1024
