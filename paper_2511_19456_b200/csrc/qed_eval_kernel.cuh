@@ -17,19 +17,26 @@
 
 namespace qed {
 
-// ---- shared-memory spinor layouts (gen/lower.py aos_slot / swz)
-__device__ __forceinline__ int aos_slot(int off, int c) { return off + 2 * (c ^ ((off >> 4) & 3)); }
+// ---- shared-memory spinor layouts (gen/lower.py aos_slot / swz): interior spinors have a pitch of SP
+// doubles; SP = 10: components contiguous; SP = 8: component c at 16-byte slot c ^ ((off >> 4) & 3)
+template <int SP>
+__device__ __forceinline__ int aos_slot(int off, int c) {
+  if constexpr (SP == 8) return off + 2 * (c ^ ((off >> 4) & 3));
+  else return off + 2 * c;
+}
 __device__ __forceinline__ int swz(int h) { return (h & ~7) | ((h + (h >> 3)) & 7); }
 
+template <int SP>
 __device__ __forceinline__ spinor ld_aos(const double* base, int off) {
   spinor s;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) s.v[c] = ld2(base + aos_slot(off, c));
+  for (int c = 0; c < 4; ++c) s.v[c] = ld2(base + aos_slot<SP>(off, c));
   return s;
 }
+template <int SP>
 __device__ __forceinline__ void st_aos(double* base, int off, const spinor& s) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) st2(base + aos_slot(off, c), s.v[c]);
+  for (int c = 0; c < 4; ++c) st2(base + aos_slot<SP>(off, c), s.v[c]);
 }
 template <int NH>
 __device__ __forceinline__ void st_leaf(double* base, int region, int idx, const spinor& s) {
@@ -55,27 +62,27 @@ struct Tasks {
     double e[3], m[5];
     ld_eps(b + t.y, e);
     ld_mask(b + t.z, m);
-    st_aos(b, t.w, prop_col(m, eslash_col(e, ld_aos(b, t.x))));
+    st_aos<T::SP>(b, t.w, prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x))));
   }
   // out-side V+S1 (interior): out = (parent epsslash) S(Q)
   static __device__ __forceinline__ void vs_row(double* b, ushort4 t) {
     double e[3], m[5];
     ld_eps(b + t.y, e);
     ld_mask(b + t.z, m);
-    st_aos(b, t.w, prop_row(m, eslash_row(e, ld_aos(b, t.x))));
+    st_aos<T::SP>(b, t.w, prop_row(m, eslash_row(e, ld_aos<T::SP>(b, t.x))));
   }
   // in-side leaf: phi = S(Q_A) epsslash parent  (V + the propagation half of S2)
   static __device__ __forceinline__ void phi(double* b, ushort4 t) {
     double e[3], m[5];
     ld_eps(b + t.y, e);
     ld_mask(b + t.z, m);
-    st_leaf<T::NHI>(b, T::PHI, t.w, prop_col(m, eslash_col(e, ld_aos(b, t.x))));
+    st_leaf<T::NHI>(b, T::PHI, t.w, prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x))));
   }
   // out-side leaf: ubar = parent epsslash
   static __device__ __forceinline__ void ub(double* b, ushort4 t) {
     double e[3];
     ld_eps(b + t.y, e);
-    st_leaf<T::NHO>(b, T::UBL, t.w, eslash_row(e, ld_aos(b, t.x)));
+    st_leaf<T::NHO>(b, T::UBL, t.w, eslash_row(e, ld_aos<T::SP>(b, t.x)));
   }
 };
 
@@ -93,12 +100,12 @@ struct BGTasks {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double e[3];
     ld_eps(b + d[3], e);
-    spinor acc = ROW ? eslash_row(e, ld_aos(b, d[2])) : eslash_col(e, ld_aos(b, d[2]));
+    spinor acc = ROW ? eslash_row(e, ld_aos<T::SP>(b, d[2])) : eslash_col(e, ld_aos<T::SP>(b, d[2]));
 #pragma unroll
     for (int q = 1; q < K; ++q) {
       ld_eps(b + d[3 + 2 * q], e);
-      if (ROW) eslash_row_acc(e, ld_aos(b, d[2 + 2 * q]), acc);
-      else eslash_col_acc(e, ld_aos(b, d[2 + 2 * q]), acc);
+      if (ROW) eslash_row_acc(e, ld_aos<T::SP>(b, d[2 + 2 * q]), acc);
+      else eslash_col_acc(e, ld_aos<T::SP>(b, d[2 + 2 * q]), acc);
     }
     return acc;
   }
@@ -107,14 +114,14 @@ struct BGTasks {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
-    st_aos(b, d[1], prop_col(m, vsum<K, false>(b, raw)));
+    st_aos<T::SP>(b, d[1], prop_col(m, vsum<K, false>(b, raw)));
   }
   template <int K>
   static __device__ __forceinline__ void out_node(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
-    st_aos(b, d[1], prop_row(m, vsum<K, true>(b, raw)));
+    st_aos<T::SP>(b, d[1], prop_row(m, vsum<K, true>(b, raw)));
   }
   // leaf descriptor field out = lb * 1024 + h: helicity h of the lb-th subset of the batch
   template <int K>
@@ -227,8 +234,8 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
     spinor u0, u1;
     u0.v[0] = {nn, 0}; u0.v[1] = {0, 0}; u0.v[2] = {sg * p[3] * r, 0}; u0.v[3] = {sg * p[1] * r, p[2] * r};
     u1.v[0] = {0, 0}; u1.v[1] = {nn, 0}; u1.v[2] = {sg * p[1] * r, -p[2] * r}; u1.v[3] = {-sg * p[3] * r, 0};
-    st_aos(base, g == 0 ? T::U : T::UB, u0);
-    st_aos(base, (g == 0 ? T::U : T::UB) + 8, u1);
+    st_aos<T::SP>(base, g == 0 ? T::U : T::UB, u0);
+    st_aos<T::SP>(base, (g == 0 ? T::U : T::UB) + T::SP, u1);
   }
 }
 

@@ -123,7 +123,7 @@ __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, se
 // interior levels <= {plan.store} stored per point, {plan.stride * 8} B shared memory per point
 struct T {{
   static constexpr int N = {N}, J = {plan.j}, G = {plan.G};
-  static constexpr int STRIDE = {plan.stride};
+  static constexpr int STRIDE = {plan.stride}, SP = {plan.sp};
   static constexpr int {lay};
   static constexpr int NSIG = {plan.n_sigma}, NTAU = {plan.n_tau}, NHI = {plan.n_hi}, NHO = {plan.n_ho};
   static constexpr int NSETS = {len(plan.sets)}, SETB = 1, LEAFB = 0;

@@ -116,7 +116,7 @@ __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, se
 
 struct T {{
   static constexpr int N = {N}, J = {plan.j}, G = {plan.G}, DW = {plan.dw};
-  static constexpr int STRIDE = {plan.stride};
+  static constexpr int STRIDE = {plan.stride}, SP = {plan.sp};
   static constexpr int {lay};
   static constexpr int NSIG = 1, NTAU = 1, NHI = {plan.n_hi}, NHO = {plan.n_ho};
   static constexpr int NSETS = {len(plan.sets)}, SETB = {B}, LEAFB = {L['LEAFB']};

@@ -55,11 +55,11 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
 
     def put_aos(off, v):
         for c in range(4):
-            o = aos_slot(off, c)
+            o = aos_slot(off, c, plan.sp)
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
     def get_aos(off):
-        return np.array([complex(sm[aos_slot(off, c)], sm[aos_slot(off, c) + 1]) for c in range(4)])
+        return np.array([complex(sm[aos_slot(off, c, plan.sp)], sm[aos_slot(off, c, plan.sp) + 1]) for c in range(4)])
 
     def put_leaf(base, nh, idx, v):
         row, h = divmod(idx, nh)
@@ -84,10 +84,10 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         sm[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
     n = math.sqrt(p[0] + 1)
     put_aos(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
-    put_aos(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
+    put_aos(L["U"] + plan.sp, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
     n = math.sqrt(pp[0] + 1)
     put_aos(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
-    put_aos(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
+    put_aos(L["UB"] + plan.sp, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
     for m in range(1, (1 << N) - 1):
         Q = p.copy()
         for i in range(N):
@@ -153,11 +153,11 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
 
     def put_aos(off, v):
         for c in range(4):
-            o = aos_slot(off, c)
+            o = aos_slot(off, c, plan.sp)
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
     def get_aos(off):
-        return np.array([complex(sm[aos_slot(off, c)], sm[aos_slot(off, c) + 1]) for c in range(4)])
+        return np.array([complex(sm[aos_slot(off, c, plan.sp)], sm[aos_slot(off, c, plan.sp) + 1]) for c in range(4)])
 
     LB = L["LEAFB"]
 
@@ -186,10 +186,10 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         sm[L["EPS"] + i * 8 + 4: L["EPS"] + i * 8 + 7] = (-sf, cf, 0.0)
     n = math.sqrt(p[0] + 1)
     put_aos(L["U"], np.array([n, 0, p[3] / n, (p[1] + 1j * p[2]) / n]))
-    put_aos(L["U"] + 8, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
+    put_aos(L["U"] + plan.sp, np.array([0, n, (p[1] - 1j * p[2]) / n, -p[3] / n]))
     n = math.sqrt(pp[0] + 1)
     put_aos(L["UB"], np.array([n, 0, -pp[3] / n, -(pp[1] - 1j * pp[2]) / n]))
-    put_aos(L["UB"] + 8, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
+    put_aos(L["UB"] + plan.sp, np.array([0, n, -(pp[1] + 1j * pp[2]) / n, pp[3] / n]))
     for m in range(1, (1 << N) - 1):
         Q = p.copy()
         for i in range(N):

@@ -29,8 +29,8 @@ Static schedule (one device), one group of G = 2^N lanes per 
 Lane g owns the 4 configurations (s, s') x fixed (lam_0..lam_{N-1}) = bits of g.
 
 Shared-memory spinor layouts (bank-conflict free for the access patterns):
-  interior / external spinors: 8 doubles, component c stored at 16-byte slot c ^ ((idx >> 1) & 3),
-      idx = spinor index = offset / 8;
+  interior / external spinors: 4 complex components contiguous, pitch SP = 10 doubles (80 B: consecutive
+      spinors written by consecutive lanes fall in distinct bank slots, no address arithmetic);
   leaves: component-major rows  [sigma][c][hi'] / [tau][c][ho'], hi' = swz(hi) (see swz()).
 """
 from __future__ import annotations
@@ -58,10 +58,25 @@ def swz(h: int) -> int:
     return (h & ~7) | ((h + (h >> 3)) & 7)
 
 
-def aos_slot(off: int, c: int) -> int:
-    """Double offset of component c of the interior spinor starting at `off` (multiple of 8)."""
-    assert off % 8 == 0
-    return off + 2 * (c ^ ((off >> 4) & 3))
+SP = 10   # default spinor pitch (doubles) for plans that do not choose one
+
+
+def aos_slot(off: int, c: int, sp: int = SP) -> int:
+    """Double offset of component c of the interior spinor starting at `off`.
+    sp = 10: components contiguous, 80-byte pitch (8 consecutive spinors hit 8 distinct 16-byte bank slots,
+    no address arithmetic); sp = 8: 64-byte pitch, component c at slot c ^ ((off >> 4) & 3) (same bank
+    property, 20 % less shared memory, 4 integer ops per component)."""
+    if sp == 8:
+        assert off % 8 == 0
+        return off + 2 * (c ^ ((off >> 4) & 3))
+    assert off % 2 == 0
+    return off + 2 * c
+
+
+# measured per process size (profiles/sweep_r12.jsonl vs r10/r11): the 80-byte pitch wins where the kernel
+# is issue-bound, the 64-byte pitch where shared memory limits occupancy
+PITCH_CDAG = {2: 8, 3: 8, 4: 8, 5: 10, 6: 8}
+PITCH_BG = {2: 8, 3: 8, 4: 10, 5: 8, 6: 8, 7: 8, 8: 10, 9: 10}
 
 
 @dataclass
@@ -118,7 +133,7 @@ def default_store(N: int, j: int) -> int:
     return 1 if N >= 6 else max(j, N - j)
 
 
-def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
+def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | None = None) -> Plan:
     if N < 2:
         raise ValueError("need at least two photons (n >= 1)")
     if j is None:
@@ -128,6 +143,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
         store = default_store(N, j)
     G = 1 << N
     full = (1 << N) - 1
+    SP = sp if sp is not None else PITCH_CDAG.get(N, 10)
 
     lay: dict[str, int] = {}
     off = 0
@@ -142,25 +158,25 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
     alloc("RED", max(2, G // 32))    # cross-warp reduction scratch (groups of > 32 lanes)
     alloc("EPS", N * 2 * 4)          # [photon][lam][e1, e2, e3, pad]
     alloc("MASK", (1 << N) * 6)      # [subset][Qp, Qm, qx, qy, qz, pad]
-    alloc("U", 2 * 8, 8)             # [s] spinor (AoS, swizzled)
-    alloc("UB", 2 * 8, 8)            # [s'] spinor
+    alloc("U", 2 * SP, 8)             # [s] spinor (AoS, swizzled)
+    alloc("UB", 2 * SP, 8)            # [s'] spinor
     in_nodes: dict[int, dict[tuple, int]] = {}
     out_nodes: dict[int, dict[tuple, int]] = {}
     for i in range(1, min(j, store + 1)):
         pre = _prefixes_in(range(N), i)
-        alloc(f"IN{i}", len(pre) * (1 << (i + 1)) * 8, 8)
+        alloc(f"IN{i}", len(pre) * (1 << (i + 1)) * SP, 8)
         in_nodes[i] = {p: k for k, p in enumerate(pre)}
     for i in range(1, min(N - j, store + 1)):
         pre = _prefixes_in(range(N), i)
-        alloc(f"OUT{i}", len(pre) * (1 << (i + 1)) * 8, 8)
+        alloc(f"OUT{i}", len(pre) * (1 << (i + 1)) * SP, 8)
         out_nodes[i] = {p: k for k, p in enumerate(pre)}
     # per-set recomputed interior levels: prefixes of length i inside a set of size j / N-j
     set_in_nodes: dict[int, dict[tuple, int]] = {}
     set_out_nodes: dict[int, dict[tuple, int]] = {}
     for i in range(store + 1, j):
-        alloc(f"SIN{i}", perm_count(j, i) * (1 << (i + 1)) * 8, 8)
+        alloc(f"SIN{i}", perm_count(j, i) * (1 << (i + 1)) * SP, 8)
     for i in range(store + 1, N - j):
-        alloc(f"SOUT{i}", perm_count(N - j, i) * (1 << (i + 1)) * 8, 8)
+        alloc(f"SOUT{i}", perm_count(N - j, i) * (1 << (i + 1)) * SP, 8)
     n_sigma, n_tau = math.factorial(j), math.factorial(N - j)
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
     alloc("PHI", n_sigma * 4 * n_hi * 2, 8)
@@ -185,28 +201,29 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
         return m
 
     plan = Plan(N=N, j=j, G=G, store=store, sets=[], sigmas=[], taus=[], layout=lay, stride=stride)
+    plan.sp = SP
 
     # ---------------------------------------------------------------- stored interior levels (V+S1 fused)
     def in_off(prefix, h, set_local=None):
         i = len(prefix)
         if i in in_nodes:
-            return lay[f"IN{i}"] + (in_nodes[i][prefix] * (1 << (i + 1)) + h) * 8
-        return lay[f"SIN{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * 8
+            return lay[f"IN{i}"] + (in_nodes[i][prefix] * (1 << (i + 1)) + h) * SP
+        return lay[f"SIN{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * SP
 
     def out_off(prefix, h, set_local=None):
         i = len(prefix)
         if i in out_nodes:
-            return lay[f"OUT{i}"] + (out_nodes[i][prefix] * (1 << (i + 1)) + h) * 8
-        return lay[f"SOUT{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * 8
+            return lay[f"OUT{i}"] + (out_nodes[i][prefix] * (1 << (i + 1)) + h) * SP
+        return lay[f"SOUT{i}"] + (set_local[prefix] * (1 << (i + 1)) + h) * SP
 
     def in_task(pre, h, local=None):
         i = len(pre)
-        parent = lay["U"] + (h & 1) * 8 if i == 1 else in_off(pre[:-1], h & ((1 << i) - 1), local)
+        parent = lay["U"] + (h & 1) * SP if i == 1 else in_off(pre[:-1], h & ((1 << i) - 1), local)
         return (parent, eps_off(pre[-1], (h >> i) & 1), mask_off(mask_of(pre)), in_off(pre, h, local))
 
     def out_task(pre, h, local=None):
         i = len(pre)
-        parent = lay["UB"] + (h & 1) * 8 if i == 1 else out_off(pre[:-1], h & ((1 << i) - 1), local)
+        parent = lay["UB"] + (h & 1) * SP if i == 1 else out_off(pre[:-1], h & ((1 << i) - 1), local)
         return (parent, eps_off(pre[-1], (h >> i) & 1), mask_off(full & ~mask_of(pre)), out_off(pre, h, local))
 
     for i in sorted(in_nodes):
@@ -253,7 +270,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
             for hi in range(n_hi):
                 lam = {x: (hi >> pos[x]) & 1 for x in A}
                 hpar = (hi & 1) | sum(lam[sg[l]] << (l + 1) for l in range(j - 1))
-                parent = lay["U"] + (hi & 1) * 8 if j == 1 else in_off(sg[:-1], hpar, local_in)
+                parent = lay["U"] + (hi & 1) * SP if j == 1 else in_off(sg[:-1], hpar, local_in)
                 phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)), si * n_hi + hi))
         ub = []
         L = N - j
@@ -261,7 +278,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None) -> Plan:
             for ho in range(n_ho):
                 lam = {x: (ho >> pos[x]) & 1 for x in Ac}
                 hpar = (ho & 1) | sum(lam[tu[l]] << (l + 1) for l in range(L - 1))
-                parent = lay["UB"] + (ho & 1) * 8 if L == 1 else out_off(tu[:-1], hpar, local_out)
+                parent = lay["UB"] + (ho & 1) * SP if L == 1 else out_off(tu[:-1], hpar, local_out)
                 ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, ti * n_ho + ho))
         stages.append([("phi", phi), ("ub", ub)])
         plan.set_stages.append(stages)

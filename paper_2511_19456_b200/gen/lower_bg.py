@@ -26,7 +26,7 @@ import math
 from dataclasses import dataclass, field
 
 from .dag import balanced_split
-from .lower import FLOPS
+from .lower import FLOPS, PITCH_BG
 
 FLOPS_BG = dict(FLOPS)
 FLOPS_BG["VACC"] = 48    # accumulating vertex: 8 real outputs x 3 fma
@@ -98,12 +98,14 @@ def default_bg_store(N: int, j: int) -> int:
     return N if spinors(N) * 64 <= 110 * 1024 else 2
 
 
-def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None) -> BGPlan:
+def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None,
+                 sp: int | None = None) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
     G = 1 << N
     full = (1 << N) - 1
+    SP = sp if sp is not None else PITCH_BG.get(N, 10)
     if store is None:
         store = default_bg_store(N, j)
     recompute = store + 1 < max(j, N - j)
@@ -122,23 +124,23 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     alloc("RED", max(2, G // 32))
     alloc("EPS", N * 2 * 4)
     alloc("MASK", (1 << N) * 6)
-    alloc("U", 16, 8)
-    alloc("UB", 16, 8)
+    alloc("U", 2 * SP, 8)
+    alloc("UB", 2 * SP, 8)
     in_idx: dict[int, dict[tuple, int]] = {}
     out_idx: dict[int, dict[tuple, int]] = {}
     for k in range(1, min(j, store + 1)):
         subs = _subsets(N, k)
-        alloc(f"IN{k}", len(subs) * (1 << (k + 1)) * 8, 8)
+        alloc(f"IN{k}", len(subs) * (1 << (k + 1)) * SP, 8)
         in_idx[k] = {s: i for i, s in enumerate(subs)}
     for k in range(1, min(N - j, store + 1)):
         subs = _subsets(N, k)
-        alloc(f"OUT{k}", len(subs) * (1 << (k + 1)) * 8, 8)
+        alloc(f"OUT{k}", len(subs) * (1 << (k + 1)) * SP, 8)
         out_idx[k] = {s: i for i, s in enumerate(subs)}
     # per-subset recomputed levels: subsets of size k inside A (|A| = j) / inside A^c (|A^c| = N - j)
     for k in range(store + 1, j):
-        alloc(f"SIN{k}", setb * math.comb(j, k) * (1 << (k + 1)) * 8, 8)
+        alloc(f"SIN{k}", setb * math.comb(j, k) * (1 << (k + 1)) * SP, 8)
     for k in range(store + 1, N - j):
-        alloc(f"SOUT{k}", setb * math.comb(N - j, k) * (1 << (k + 1)) * 8, 8)
+        alloc(f"SOUT{k}", setb * math.comb(N - j, k) * (1 << (k + 1)) * SP, 8)
     set_local: dict[tuple, int] = {}
     cur_slot = [0]
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
@@ -168,13 +170,13 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     def node_off(side, S, h):
         k = len(S)
         if k == 0:
-            return (lay["U"] if side == "in" else lay["UB"]) + h * 8
+            return (lay["U"] if side == "in" else lay["UB"]) + h * SP
         if k > store:
             idx = set_local[(side, S)]
             slot = cur_slot[0] * math.comb(j if side == "in" else N - j, k)   # this subset's batch slot
-            return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + ((slot + idx) * (1 << (k + 1)) + h) * 8
+            return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + ((slot + idx) * (1 << (k + 1)) + h) * SP
         idx = (in_idx if side == "in" else out_idx)[k][S]
-        return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (idx * (1 << (k + 1)) + h) * 8
+        return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (idx * (1 << (k + 1)) + h) * SP
 
     def task(side, S, h, out, mask):
         """descriptor for node (S, h): sum over i in S of parent (S \\ i) x eps_i."""
@@ -187,6 +189,7 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         return d
 
     plan = BGPlan(N=N, j=j, G=G, sets=[], layout=lay, stride=stride)
+    plan.sp = SP
     plan.setb = setb
     plan.store = store
     plan.set_stages = []
