@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {
           const unsigned h = T::config_of(idx, sub);
+          if (h == 0xffffffffu) continue;   // duplicate holder of this amplitude (split bodies)
           unsigned hx = 0;
 #pragma unroll
           for (int b = 0; b < N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
       if (a.fixed_mask == 0) {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) sum = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], sum));
+        if (T::config_of(0, sub) == 0xffffffffu) sum = 0.0;
       } else {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {

@@ -291,7 +291,7 @@ def emit_regs_source(N: int) -> str:
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, false>;"
         for i, (d, w, m, p) in enumerate(vs))
-    tpp = "{" + ", ".join("4" if d == "T4" else "2" for d, *_ in vs) + "}"
+    tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "2" for d, *_ in vs) + "}"
     body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) if N == 3 else ""
     t4 = f"""
 // four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
