@@ -270,8 +270,9 @@ def run_mc(args, world, rank, stream, dev) -> dict:
     return out
 
 
-def sweep_per_n(args, world, stream, dev, algorithm: str) -> dict:
-    """Every process size n = 1..5 at its own batch size, same timing protocol, 5 steps."""
+def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool = False) -> dict:
+    """Every process size at its own batch size, same timing protocol, 5 steps.  paper_direction:
+    e- gamma^n -> e- gamma (time-reversed RAMBO kinematics), same kernels."""
     import torch
 
     import synthetic
@@ -279,8 +280,10 @@ def sweep_per_n(args, world, stream, dev, algorithm: str) -> dict:
     out = {}
     for m in range(1, 9 if algorithm == "bg" else 6):
         Pm = PER_N_POINTS[m] * (4 if algorithm == "bg" and 4 <= m <= 5 else 1)
-        pm = qed.Process(m, algorithm=algorithm)
+        pm = qed.Process(m, n_in_photons=m if paper_direction else 1, algorithm=algorithm)
         mm = synthetic.rambo_cm(m, Pm, sqrt_s=args.sqrt_s, seed=7 + m, device=dev)
+        if paper_direction:   # initial <-> final: e_in' = e_out, gamma_in' = gamma_out..., e_out' = e_in, gamma_out' = gamma_in
+            mm = torch.cat([mm[:, 2:3], mm[:, 3:], mm[:, 0:1], mm[:, 1:2]], dim=1)
         sm = synthetic.to_soa(mm)
         del mm
         om = torch.empty(Pm, dtype=torch.float64, device=dev)
@@ -361,10 +364,11 @@ def run_b200(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, world, proc, soa, P)
-    per_n = per_n_bg = None
+    per_n = per_n_bg = per_n_paper = None
     if not args.no_per_n:
         per_n = sweep_per_n(args, world, stream, dev, "cdag")
         per_n_bg = sweep_per_n(args, world, stream, dev, "bg")
+        per_n_paper = sweep_per_n(args, world, stream, dev, "cdag", paper_direction=True)
 
     mc_res = None if args.no_mc else run_mc(args, world, rank, stream, dev)
 
@@ -389,7 +393,7 @@ def run_b200(args, world, rank, local):
                                                             "grid_blocks")}, variant=os.environ.get("QED_VARIANT", "0"))},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "fp64_dfma_microbench": peak, "per_n": per_n,
-            "per_n_berends_giele": per_n_bg, "mc": mc_res,
+            "per_n_berends_giele": per_n_bg, "per_n_paper_direction": per_n_paper, "mc": mc_res,
         }
         print(json.dumps(line), flush=True)
 
