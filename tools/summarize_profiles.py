@@ -81,7 +81,7 @@ for name in sorted(os.listdir(src)):
         b = rd * scale.get(ui["dram__bytes_read.sum"], 1) + wr * scale.get(ui["dram__bytes_write.sum"], 1)
         log = open(os.path.join(src, name.replace(".ncu-rep", ".log"))).read() if os.path.exists(
             os.path.join(src, name.replace(".ncu-rep", ".log"))) else ""
-        pts = {"n2": 4194304, "n5": 262144}.get(case)
+        pts = {"n2": 4194304, "n5": 262144, "bg5": 1048576}.get(case)
         if pts:
             traffic[f"{case}_points{pts}"] = int(b)
     print("wrote", os.path.join(dst, f"full_{case}.txt"))
