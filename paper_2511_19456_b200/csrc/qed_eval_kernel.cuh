@@ -243,9 +243,10 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
 // acc[c & 1][s | s' << 1] += sum_{sigma, tau} ubar_tau[ho + s'] . phi_sigma[hi + s]
 // phi of one sigma stays in registers across the tau loop; loops are rolled so that ptxas
 // cannot hoist every leaf load of the subset (which spills).
+// hh: packed (2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1)) of this lane and subset (gen tables)
 template <class T, int AS>
-__device__ __forceinline__ void join_set(const double* __restrict__ base, int hi, int ho, double (&acc)[AS][8], int lb = 0) {
-  const int h0 = 2 * swz(hi), h1 = 2 * swz(hi + 1), o0 = 2 * swz(ho), o1 = 2 * swz(ho + 1);
+__device__ __forceinline__ void join_set(const double* __restrict__ base, unsigned hh, double (&acc)[AS][8], int lb = 0) {
+  const int h0 = hh & 255, h1 = (hh >> 8) & 255, o0 = (hh >> 16) & 255, o1 = hh >> 24;
   base += lb * T::LEAFB;   // leaf buffer of the lb-th subset of a batch (T::SETB subsets per stage)
 #pragma unroll 1
   for (int sg = 0; sg < T::NSIG; ++sg) {
@@ -299,18 +300,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     T::run_set(base, g, pb, s0);      // leaves of subsets s0 .. s0 + SETB - 1
     group_sync<T>(pb);
 #pragma unroll
-    for (int lb = 0; lb < T::SETB; ++lb) {
-      const int si = s0 + lb;
-      int hi = 0, ho = 0;
-      const unsigned inA = T::set_mask(si);
-#pragma unroll
-      for (int i = 0; i < T::N; ++i) {
-        const int lam = (g >> i) & 1;
-        if ((inA >> i) & 1) hi |= lam << T::set_pos(si, i);
-        else ho |= lam << T::set_pos(si, i);
-      }
-      join_set<T, AS>(base, hi, ho, acc, lb);
-    }
+    for (int lb = 0; lb < T::SETB; ++lb) join_set<T, AS>(base, T::hiho(s0 + lb, g), acc, lb);
     group_sync<T>(pb);
   }
 #pragma unroll

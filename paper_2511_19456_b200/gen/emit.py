@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import os
 
-from .lower import Plan, make_plan
+from .lower import Plan, hiho_table, make_plan
 
 SMEM_PER_SM = 228 * 1024
 SMEM_RESERVED_PER_BLOCK = 1024
@@ -110,6 +110,7 @@ def emit_plan_namespace(plan: Plan, ns: str) -> str:
     run_set = "\n".join(lines)
     set_pos = [p for ps in plan.set_pos for p in ps]
     set_mask = [sum(1 << x for x in A) for A in plan.sets]
+    hiho = hiho_table(plan)
     for tbl in (in_flat, out_flat, set_flat):
         for t in tbl:
             assert max(t) < 65536
@@ -119,6 +120,8 @@ def emit_plan_namespace(plan: Plan, ns: str) -> str:
 {_tasks("k_in_tasks", in_flat)}{_tasks("k_out_tasks", out_flat)}{_tasks("k_set_tasks", set_flat)}
 __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str, set_pos))}}};
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
+// per (subset, lane): packed 2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1) (leaf-row offsets of the lane's tile)
+__device__ const unsigned k_hiho[{len(hiho)}] = {{{", ".join(f"0x{x:08x}u" for x in hiho)}}};
 
 // interior levels <= {plan.store} stored per point, {plan.stride * 8} B shared memory per point
 struct T {{
@@ -130,6 +133,7 @@ struct T {{
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
+  static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
   static __device__ __forceinline__ void run_interiors(double* base, int g, int pb) {{
 {interiors}
   }}

@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 
 from .emit import choose_launch, lane_offset
+from .lower import hiho_table
 from .lower_bg import BGPlan, make_bg_plan
 
 
@@ -87,6 +88,7 @@ def emit_bg_source(plan: BGPlan) -> str:
                f"k_sets + (si / {B}) * {per_set} + {n_rec + n_in}, qed::BGFn<T, {N - plan.j}, 3>{{}});")
     set_pos = [p for ps in plan.set_pos for p in ps]
     set_mask = [sum(1 << x for x in A) for A in plan.sets]
+    hiho = hiho_table(plan)
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in plan.flops.items())
     lay = ", ".join(f"{k} = {L[k]}" for k in ("MOM", "RED", "EPS", "MASK", "U", "UB", "PHI", "UBL"))
     variant_structs = "".join(f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }};\n"
@@ -113,6 +115,8 @@ namespace {ns} {{
 {_tbl("k_levels", lev_flat, plan.dw)}{_tbl("k_sets", set_flat, plan.dw)}
 __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str, set_pos))}}};
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
+// per (subset, lane): packed 2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1) (leaf-row offsets of the lane's tile)
+__device__ const unsigned k_hiho[{len(hiho)}] = {{{", ".join(f"0x{x:08x}u" for x in hiho)}}};
 
 struct T {{
   static constexpr int N = {N}, J = {plan.j}, G = {plan.G}, DW = {plan.dw};
@@ -123,6 +127,7 @@ struct T {{
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
+  static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
   static __device__ __forceinline__ void run_interiors(double* base, int g, int pb) {{
 {interiors}
   }}

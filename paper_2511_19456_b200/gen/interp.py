@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from .lower import Plan, aos_slot, swz
+from .lower import Plan, aos_slot, hiho_table, swz
 
 ALPHA = 1 / 137.035999084
 
@@ -48,6 +48,14 @@ def _prop_row(mk, v):
     return np.array([qp * a + bK[0], qp * b + bK[1], -tK[0] + qm * c, -tK[1] + qm * d])
 
 
+def _join_offsets(hiho, si, G, h, N):
+    """Leaf-row offsets (in doubles, swizzle applied) of amplitude index h for subset si, from the
+    per-(subset, lane) table the kernels read (lane g = the photon-polarisation bits of h)."""
+    w = hiho[si * G + ((h >> 1) & (G - 1))]
+    s, sp = h & 1, (h >> (N + 1)) & 1
+    return (w >> (8 * s)) & 255, (w >> (16 + 8 * sp)) & 255
+
+
 def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     """All helicity amplitudes (external bit order, with e^N) at one point, via the tables."""
     N, L = plan.N, plan.layout
@@ -66,6 +74,12 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         for c in range(4):
             o = base + ((row * 4 + c) * nh + swz(h)) * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
+
+    hiho = hiho_table(plan)
+
+    def get_leaf_off(base, nh, row, o2):
+        o = base + row * 4 * nh * 2 + o2
+        return np.array([complex(sm[o + c * nh * 2], sm[o + c * nh * 2 + 1]) for c in range(4)])
 
     def get_leaf(base, nh, row, h):
         return np.array([complex(sm[base + ((row * 4 + c) * nh + swz(h)) * 2],
@@ -124,16 +138,12 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         for stage in plan.set_stages[si]:
             for kind, tasks in stage:
                 run(kind, tasks)
-        Ac = [x for x in range(N) if x not in A]
-        pos = plan.set_pos[si]
         for h in range(H):
-            s, sp = h & 1, (h >> (N + 1)) & 1
-            hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
-            ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
+            oi, oo = _join_offsets(hiho, si, plan.G, h, N)
             for a in range(plan.n_sigma):
-                phi = get_leaf(L["PHI"], plan.n_hi, a, hi)
+                phi = get_leaf_off(L["PHI"], plan.n_hi, a, oi)
                 for b in range(plan.n_tau):
-                    amp[h] += get_leaf(L["UBL"], plan.n_ho, b, ho) @ phi
+                    amp[h] += get_leaf_off(L["UBL"], plan.n_ho, b, oo) @ phi
     e_n = math.sqrt(4 * math.pi * ALPHA) ** N
     out = np.zeros(H, dtype=complex)
     e_out = n_in_ph + 1
@@ -167,6 +177,12 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         for c in range(4):
             o = base + (c * nh + swz(h)) * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
+
+    hiho = hiho_table(plan)
+
+    def get_leaf_off(base, nh, o2, lb=0):
+        o = base + lb * LB + o2
+        return np.array([complex(sm[o + c * nh * 2], sm[o + c * nh * 2 + 1]) for c in range(4)])
 
     def get_leaf(base, nh, h, lb=0):
         base += lb * LB
@@ -232,13 +248,9 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
                     put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
                 for d in plan.set_out[sj]:
                     put_leaf(L["UBL"], plan.n_ho, d[1], vsum(d, True))
-        Ac = [x for x in range(N) if x not in A]
-        pos = plan.set_pos[si]
         for h in range(H):
-            s, sp = h & 1, (h >> (N + 1)) & 1
-            hi = s | sum(((h >> (1 + x)) & 1) << pos[x] for x in A)
-            ho = sp | sum(((h >> (1 + x)) & 1) << pos[x] for x in Ac)
-            amp[h] += get_leaf(L["UBL"], plan.n_ho, ho, lb) @ get_leaf(L["PHI"], plan.n_hi, hi, lb)
+            oi, oo = _join_offsets(hiho, si, plan.G, h, N)
+            amp[h] += get_leaf_off(L["UBL"], plan.n_ho, oo, lb) @ get_leaf_off(L["PHI"], plan.n_hi, oi, lb)
     e_n = math.sqrt(4 * math.pi * ALPHA) ** N
     out = np.zeros(H, dtype=complex)
     e_out = n_in_ph + 1

@@ -318,3 +318,24 @@ def trie_node_counts(plan: Plan) -> dict[str, int]:
     S1 = sum(perm_count(N, i) for i in range(1, j)) + sum(perm_count(N, i) for i in range(1, N - j))
     S2 = sum(len(s) * len(t) for s, t in zip(plan.sigmas, plan.taus))
     return {"V": V, "S1": S1, "S2": S2}
+
+
+def hiho_table(plan) -> list[int]:
+    """Per (subset si, lane g): the lane's leaf-row offsets for the join, packed in one word:
+    2 swz(hi) | 2 swz(hi + 1) << 8 | 2 swz(ho) << 16 | 2 swz(ho + 1) << 24, with hi = s=0 | lam_A bits at
+    their positions in A, ho likewise on the complement (lam_i = bit i of g)."""
+    out = []
+    for si, A in enumerate(plan.sets):
+        pos = plan.set_pos[si]
+        for g in range(plan.G):
+            hi = ho = 0
+            for i in range(plan.N):
+                lam = (g >> i) & 1
+                if i in A:
+                    hi |= lam << pos[i]
+                else:
+                    ho |= lam << pos[i]
+            w = [2 * swz(hi), 2 * swz(hi + 1), 2 * swz(ho), 2 * swz(ho + 1)]
+            assert max(w) < 256
+            out.append(w[0] | w[1] << 8 | w[2] << 16 | w[3] << 24)
+    return out
