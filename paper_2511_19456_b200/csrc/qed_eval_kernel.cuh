@@ -38,11 +38,11 @@ __device__ __forceinline__ void st_aos(double* base, int off, const spinor& s) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) st2(base + aos_slot<SP>(off, c), s.v[c]);
 }
+// leaf spinor store: p = component 0 (gen/lower.py leaf_off), components NH (helicity columns) apart
 template <int NH>
-__device__ __forceinline__ void st_leaf(double* base, int region, int idx, const spinor& s) {
-  const int row = idx / NH, h = swz(idx % NH);
+__device__ __forceinline__ void st_leaf(double* p, const spinor& s) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) st2(base + region + ((row * 4 + c) * NH + h) * 2, s.v[c]);
+  for (int c = 0; c < 4; ++c) st2(p + c * NH * 2, s.v[c]);
 }
 __device__ __forceinline__ void ld_eps(const double* p, double (&e)[3]) {
   const double2 e01 = *reinterpret_cast<const double2*>(p);
@@ -76,13 +76,13 @@ struct Tasks {
     double e[3], m[5];
     ld_eps(b + t.y, e);
     ld_mask(b + t.z, m);
-    st_leaf<T::NHI>(b, T::PHI, t.w, prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x))));
+    st_leaf<T::NHI>(b + t.w, prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x))));
   }
   // out-side leaf: ubar = parent epsslash
   static __device__ __forceinline__ void ub(double* b, ushort4 t) {
     double e[3];
     ld_eps(b + t.y, e);
-    st_leaf<T::NHO>(b, T::UBL, t.w, eslash_row(e, ld_aos<T::SP>(b, t.x)));
+    st_leaf<T::NHO>(b + t.w, eslash_row(e, ld_aos<T::SP>(b, t.x)));
   }
 };
 
@@ -123,18 +123,18 @@ struct BGTasks {
     ld_mask(b + d[0], m);
     st_aos<T::SP>(b, d[1], prop_row(m, vsum<K, true>(b, raw)));
   }
-  // leaf descriptor field out = lb * 1024 + h: helicity h of the lb-th subset of the batch
+  // leaf descriptor field out = offset of the leaf spinor (its subset's leaf buffer, swizzled column)
   template <int K>
   static __device__ __forceinline__ void in_leaf(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
-    st_leaf<T::NHI>(b + (d[1] >> 10) * T::LEAFB, T::PHI, d[1] & 1023, prop_col(m, vsum<K, false>(b, raw)));
+    st_leaf<T::NHI>(b + d[1], prop_col(m, vsum<K, false>(b, raw)));
   }
   template <int K>
   static __device__ __forceinline__ void out_leaf(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
-    st_leaf<T::NHO>(b + (d[1] >> 10) * T::LEAFB, T::UBL, d[1] & 1023, vsum<K, true>(b, raw));
+    st_leaf<T::NHO>(b + d[1], vsum<K, true>(b, raw));
   }
 };
 

@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from .lower import Plan, aos_slot, hiho_table, swz
+from .lower import Plan, aos_slot, hiho_table
 
 ALPHA = 1 / 137.035999084
 
@@ -69,10 +69,9 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     def get_aos(off):
         return np.array([complex(sm[aos_slot(off, c, plan.sp)], sm[aos_slot(off, c, plan.sp) + 1]) for c in range(4)])
 
-    def put_leaf(base, nh, idx, v):
-        row, h = divmod(idx, nh)
+    def put_leaf(nh, off, v):     # off: the descriptor's leaf offset (component 0)
         for c in range(4):
-            o = base + ((row * 4 + c) * nh + swz(h)) * 2
+            o = off + c * nh * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
     hiho = hiho_table(plan)
@@ -80,10 +79,6 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     def get_leaf_off(base, nh, row, o2):
         o = base + row * 4 * nh * 2 + o2
         return np.array([complex(sm[o + c * nh * 2], sm[o + c * nh * 2 + 1]) for c in range(4)])
-
-    def get_leaf(base, nh, row, h):
-        return np.array([complex(sm[base + ((row * 4 + c) * nh + swz(h)) * 2],
-                                 sm[base + ((row * 4 + c) * nh + swz(h)) * 2 + 1]) for c in range(4)])
 
     photon_particle = [1 + i if i < n_in_ph else n_in_ph + 2 + (i - n_in_ph) for i in range(N)]
     sign = [1.0 if i < n_in_ph else -1.0 for i in range(N)]
@@ -124,9 +119,9 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
             elif kind == "vs_row":
                 put_aos(out, _prop_row(mask(mk), _eslash_row(eps(e), get_aos(par))))
             elif kind == "phi":
-                put_leaf(L["PHI"], plan.n_hi, out, _prop_col(mask(mk), _eslash_col(eps(e), get_aos(par))))
+                put_leaf(plan.n_hi, out, _prop_col(mask(mk), _eslash_col(eps(e), get_aos(par))))
             elif kind == "ub":
-                put_leaf(L["UBL"], plan.n_ho, out, _eslash_row(eps(e), get_aos(par)))
+                put_leaf(plan.n_ho, out, _eslash_row(eps(e), get_aos(par)))
 
     for tasks in plan.in_levels:
         run("vs_col", tasks)
@@ -171,11 +166,9 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
 
     LB = L["LEAFB"]
 
-    def put_leaf(base, nh, hx, v):
-        base += (hx >> 10) * LB
-        h = hx & 1023
+    def put_leaf(nh, off, v):     # off: the descriptor's leaf offset (component 0)
         for c in range(4):
-            o = base + (c * nh + swz(h)) * 2
+            o = off + c * nh * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
     hiho = hiho_table(plan)
@@ -183,11 +176,6 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     def get_leaf_off(base, nh, o2, lb=0):
         o = base + lb * LB + o2
         return np.array([complex(sm[o + c * nh * 2], sm[o + c * nh * 2 + 1]) for c in range(4)])
-
-    def get_leaf(base, nh, h, lb=0):
-        base += lb * LB
-        return np.array([complex(sm[base + (c * nh + swz(h)) * 2], sm[base + (c * nh + swz(h)) * 2 + 1])
-                         for c in range(4)])
 
     photon_particle = [1 + i if i < n_in_ph else n_in_ph + 2 + (i - n_in_ph) for i in range(N)]
     sign = [1.0 if i < n_in_ph else -1.0 for i in range(N)]
@@ -245,9 +233,9 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
                                 put_aos(d[1], _prop_row(sm[d[0]: d[0] + 5], vsum(d, True)))
             for sj in range(si, si + plan.setb):
                 for d in plan.set_in[sj]:
-                    put_leaf(L["PHI"], plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
+                    put_leaf(plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
                 for d in plan.set_out[sj]:
-                    put_leaf(L["UBL"], plan.n_ho, d[1], vsum(d, True))
+                    put_leaf(plan.n_ho, d[1], vsum(d, True))
         for h in range(H):
             oi, oo = _join_offsets(hiho, si, plan.G, h, N)
             amp[h] += get_leaf_off(L["UBL"], plan.n_ho, oo, lb) @ get_leaf_off(L["PHI"], plan.n_hi, oi, lb)

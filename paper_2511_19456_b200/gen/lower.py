@@ -271,7 +271,8 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
                 lam = {x: (hi >> pos[x]) & 1 for x in A}
                 hpar = (hi & 1) | sum(lam[sg[l]] << (l + 1) for l in range(j - 1))
                 parent = lay["U"] + (hi & 1) * SP if j == 1 else in_off(sg[:-1], hpar, local_in)
-                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)), si * n_hi + hi))
+                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)),
+                            leaf_off(lay["PHI"], n_hi, si, hi)))
         ub = []
         L = N - j
         for ti, tu in enumerate(tau):
@@ -279,7 +280,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
                 lam = {x: (ho >> pos[x]) & 1 for x in Ac}
                 hpar = (ho & 1) | sum(lam[tu[l]] << (l + 1) for l in range(L - 1))
                 parent = lay["UB"] + (ho & 1) * SP if L == 1 else out_off(tu[:-1], hpar, local_out)
-                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, ti * n_ho + ho))
+                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, leaf_off(lay["UBL"], n_ho, ti, ho)))
         stages.append([("phi", phi), ("ub", ub)])
         plan.set_stages.append(stages)
 
@@ -318,6 +319,14 @@ def trie_node_counts(plan: Plan) -> dict[str, int]:
     S1 = sum(perm_count(N, i) for i in range(1, j)) + sum(perm_count(N, i) for i in range(1, N - j))
     S2 = sum(len(s) * len(t) for s, t in zip(plan.sigmas, plan.taus))
     return {"V": V, "S1": S1, "S2": S2}
+
+
+def leaf_off(region: int, nh: int, row: int, h: int) -> int:
+    """Offset (doubles) of component 0 of leaf spinor (row, h) in a component-major leaf region of nh
+    helicity columns; component c sits c * 2 nh further.  Leaf descriptors carry this directly."""
+    off = region + row * 4 * nh * 2 + 2 * swz(h)
+    assert off < 65536
+    return off
 
 
 def hiho_table(plan) -> list[int]:

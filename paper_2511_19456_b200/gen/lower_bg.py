@@ -26,7 +26,7 @@ import math
 from dataclasses import dataclass, field
 
 from .dag import balanced_split
-from .lower import FLOPS, PITCH_BG
+from .lower import FLOPS, PITCH_BG, leaf_off
 
 FLOPS_BG = dict(FLOPS)
 FLOPS_BG["VACC"] = 48    # accumulating vertex: 8 real outputs x 3 fma
@@ -232,8 +232,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
             stages.append(st)
         plan.set_stages.append(stages)
         lb = (len(plan.sets) - 1) % setb          # leaf buffer of this subset within its batch
-        plan.set_in.append([task("in", A, h, lb * 1024 + h, mask_off(msk(A))) for h in range(n_hi)])
-        plan.set_out.append([task("out", Ac, h, lb * 1024 + h, 0) for h in range(n_ho)])
+        phi0, ubl0 = lay["PHI"] + lb * lay["LEAFB"], lay["UBL"] + lb * lay["LEAFB"]
+        plan.set_in.append([task("in", A, h, leaf_off(phi0, n_hi, 0, h), mask_off(msk(A))) for h in range(n_hi)])
+        plan.set_out.append([task("out", Ac, h, leaf_off(ubl0, n_ho, 0, h), 0) for h in range(n_ho)])
 
     F = FLOPS_BG
     H = 1 << (N + 2)
