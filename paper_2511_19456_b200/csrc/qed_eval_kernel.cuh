@@ -300,7 +300,8 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     T::run_set(base, g, pb, s0);      // leaves of subsets s0 .. s0 + SETB - 1
     group_sync<T>(pb);
 #pragma unroll
-    for (int lb = 0; lb < T::SETB; ++lb) join_set<T, AS>(base, T::hiho(s0 + lb, g), acc, lb);
+    for (int lb = 0; lb < T::SETB; ++lb)   // padding subsets of a ragged last batch: leaves only, no join
+      if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS>(base, T::hiho(s0 + lb, g), acc, lb);
     group_sync<T>(pb);
   }
 #pragma unroll

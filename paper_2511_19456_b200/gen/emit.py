@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import os
 
-from .lower import Plan, hiho_table, make_plan
+from .lower import Plan, hiho_table, lane_offset, make_plan
 
 SMEM_PER_SM = 228 * 1024
 SMEM_RESERVED_PER_BLOCK = 1024
@@ -48,15 +48,6 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     if plan.N >= 5:   # r01 sweep: 4 partial accumulators win for n >= 4
         return [(wpb, mb4, 4, 1), (wpb, mb, 2, 1), (wpb, mb, 2, 0)]
     return [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
-
-
-def lane_offset(count_first: int, G: int) -> int:
-    """Start lane of the second task kind of a stage: right after the first kind's last lane,
-    rounded up to a warp boundary when the group spans several warps (no intra-warp divergence)."""
-    off = count_first % G
-    if G > 32 and off:
-        off = ((off + 31) // 32 * 32) % G
-    return off
 
 
 def _tasks(name, tasks):
@@ -129,7 +120,7 @@ struct T {{
   static constexpr int STRIDE = {plan.stride}, SP = {plan.sp};
   static constexpr int {lay};
   static constexpr int NSIG = {plan.n_sigma}, NTAU = {plan.n_tau}, NHI = {plan.n_hi}, NHO = {plan.n_ho};
-  static constexpr int NSETS = {len(plan.sets)}, SETB = 1, LEAFB = 0;
+  static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = NSETS, SETB = 1, LEAFB = 0;
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}

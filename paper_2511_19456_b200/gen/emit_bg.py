@@ -101,7 +101,7 @@ def emit_bg_source(plan: BGPlan) -> str:
                        for i in range(len(vs)))
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_bg.py -- do not edit.
 // Berends-Giele (distributive rewrite of the node-reduced CDAG, NEXT #1) for N = {N} photons (n = {N - 1}):
-// {len(plan.sets)} photon subsets A (|A| = j = {plan.j}), one join each, {plan.H} configurations,
+// {plan.n_sets_real} photon subsets A (|A| = j = {plan.j}; {len(plan.sets) - plan.n_sets_real} padding), one join each, {plan.H} configurations,
 // G = {plan.G} lanes per point, {B} subsets per leaf stage, {plan.stride * 8} B shared memory per point,
 // current levels <= {plan.store} stored (deeper ones recomputed per subset: +{plan.recompute_flops} executed flops);
 // variants {vs}.
@@ -123,7 +123,7 @@ struct T {{
   static constexpr int STRIDE = {plan.stride}, SP = {plan.sp};
   static constexpr int {lay};
   static constexpr int NSIG = 1, NTAU = 1, NHI = {plan.n_hi}, NHO = {plan.n_ho};
-  static constexpr int NSETS = {len(plan.sets)}, SETB = {B}, LEAFB = {L['LEAFB']};
+  static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = {plan.n_sets_real}, SETB = {B}, LEAFB = {L['LEAFB']};
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}

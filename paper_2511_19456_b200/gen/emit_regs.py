@@ -364,7 +364,7 @@ def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
     Variant 0 = best of the latest sweep (profiles/sweep_*.jsonl)."""
     if N == 3:
         return [("T", 4, 1, 2), ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2),
-                ("TI", 4, 1, 2), ("TI", 4, 1, 1)]
+                ("TI", 4, 1, 2), ("TI", 4, 1, 1), ("T", 2, 5, 1), ("T", 2, 5, 0)]
     return [("T", 2, 6, 2), ("T", 4, 1, 0), ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
 
 

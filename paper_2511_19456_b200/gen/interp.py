@@ -236,6 +236,8 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
                     put_leaf(plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
                 for d in plan.set_out[sj]:
                     put_leaf(plan.n_ho, d[1], vsum(d, True))
+        if si >= plan.n_sets_real:      # padding subset of a ragged last batch
+            continue
         for h in range(H):
             oi, oo = _join_offsets(hiho, si, plan.G, h, N)
             amp[h] += get_leaf_off(L["UBL"], plan.n_ho, oo, lb) @ get_leaf_off(L["PHI"], plan.n_hi, oi, lb)

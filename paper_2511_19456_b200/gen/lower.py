@@ -321,6 +321,15 @@ def trie_node_counts(plan: Plan) -> dict[str, int]:
     return {"V": V, "S1": S1, "S2": S2}
 
 
+def lane_offset(count_first: int, G: int) -> int:
+    """Start lane of the second task kind of a stage: right after the first kind's last lane,
+    rounded up to a warp boundary when the group spans several warps (no intra-warp divergence)."""
+    off = count_first % G
+    if G > 32 and off:
+        off = ((off + 31) // 32 * 32) % G
+    return off
+
+
 def leaf_off(region: int, nh: int, row: int, h: int) -> int:
     """Offset (doubles) of component 0 of leaf spinor (row, h) in a component-major leaf region of nh
     helicity columns; component c sits c * 2 nh further.  Leaf descriptors carry this directly."""

@@ -26,7 +26,7 @@ import math
 from dataclasses import dataclass, field
 
 from .dag import balanced_split
-from .lower import FLOPS, PITCH_BG, leaf_off
+from .lower import FLOPS, PITCH_BG, lane_offset, leaf_off
 
 FLOPS_BG = dict(FLOPS)
 FLOPS_BG["VACC"] = 48    # accumulating vertex: 8 real outputs x 3 fma
@@ -47,6 +47,7 @@ class BGPlan:
     set_out: list[list[list[int]]] = field(default_factory=list)
     set_pos: list[list[int]] = field(default_factory=list)
     flops: dict[str, int] = field(default_factory=dict)
+    n_sets_real: int = 0     # C(N, j); sets[n_sets_real:] pad the last batch to SETB subsets
 
     @property
     def H(self) -> int:
@@ -69,24 +70,85 @@ def _subsets(N, k):
     return list(itertools.combinations(range(N), k))
 
 
-def default_setb(N: int, j: int) -> int:
-    """Subsets per leaf stage: enough leaf tasks to fill the G = 2^N lanes of the group."""
-    n_sets = math.comb(N, j)
-    leaf_tasks = (1 << (j + 1)) + (1 << (N - j + 1))
-    b = 1
-    while b * 2 <= n_sets and n_sets % (b * 2) == 0 and b * leaf_tasks < (1 << N):
-        b *= 2
-    return b
+def lane_utilisation(plan) -> tuple[float, dict]:
+    """Lane-utilisation model of one point's schedule on the G lanes of its group: every barrier-
+    separated phase (interior level pair, per-batch recompute stage, leaf stage, join) lasts as long as
+    its busiest lane (task costs from FLOPS_BG; lane placement as in qed_eval_kernel.cuh run_tasks8).
+    Returns (executed flops / (G x sum of phase maxima), per-phase-kind [span, work]).  Latency is
+    ignored, so this bounds what the schedule shape allows; tools/bg_util.py prints it."""
+    F = FLOPS_BG
+    G, B, N = plan.G, plan.setb, plan.N
+
+    def cost(kind, K, leaf=False):
+        return F["V"] + (K - 1) * F["VACC"] + (F["S"] if (kind == "in" or not leaf) else 0)
+
+    def phase(groups):
+        lane = [0.0] * G
+        for cnt, c, off in groups:
+            for t in range(cnt):
+                lane[(t + off) % G] += c
+        return max(lane), sum(cnt * c for cnt, c, _ in groups)
+
+    phases = []
+    i = 0
+    while i < len(plan.levels):
+        kind, K, t = plan.levels[i]
+        grp = [(len(t), cost(kind, K), 0)]
+        if i + 1 < len(plan.levels) and plan.levels[i + 1][1] == K:
+            k2, _, t2 = plan.levels[i + 1]
+            grp.append((len(t2), cost(k2, K), lane_offset(len(t), G)))
+            i += 1
+        phases.append(("int", phase(grp)))
+        i += 1
+    for _ in range(len(plan.sets) // B):
+        for st in plan.set_stages[0]:
+            grp, prev = [], 0
+            for q, (kind, K, t) in enumerate(st):
+                grp.append((len(t) * B, cost(kind, K), lane_offset(prev, G) if q > 0 else 0))
+                prev = len(t) * B
+            phases.append(("rec", phase(grp)))
+        n_in, n_out = B * len(plan.set_in[0]), B * len(plan.set_out[0])
+        phases.append(("leaf", phase([(n_in, cost("in", plan.j, True), 0),
+                                      (n_out, cost("out", N - plan.j, True), lane_offset(n_in, G))])))
+    n_join = plan.n_sets_real * 4 * F["JOIN"]      # padding subsets skip their join
+    phases.append(("join", (float(n_join), float(n_join * G))))
+    by: dict[str, list[float]] = {}
+    for k, (m, w) in phases:
+        a = by.setdefault(k, [0.0, 0.0])
+        a[0] += m
+        a[1] += w
+    span = sum(a[0] for a in by.values())
+    return sum(a[1] for a in by.values()) / (G * span), by
 
 
-def default_setb_rec(N: int, j: int) -> int:
-    """Subsets per stage when deep levels are recomputed per subset: the largest power of two <= 4
-    that divides the number of subsets (each batched subset gets its own recompute / leaf slot)."""
+# sizes where the GPU sweep overrules the model (profiles/sweep_r18.jsonl: the modelled batch of 2 at
+# n = 2 and of 4 at n = 7 measured 3 % and 6 % slower than 1 and 2)
+SETB_MEASURED = {(3, 1): 1, (8, 4): 2}
+
+
+def default_setb(N: int, j: int, store: int, sp: int) -> int:
+    """Subsets per leaf stage (1, 2, 4 or 8, at most 4 when deep levels are recomputed per subset):
+    the batch that maximises lane utilisation x occupancy (resident warps per SM, saturating at 16).
+    It need not divide the number of subsets: the list is padded with copies of the last subset,
+    whose leaves are computed and whose joins are skipped."""
+    from .emit import choose_launch
+    if (N, j) in SETB_MEASURED:
+        return SETB_MEASURED[(N, j)]
     n_sets = math.comb(N, j)
-    b = 4
-    while n_sets % b:
-        b //= 2
-    return b
+    recompute = store + 1 < max(j, N - j)
+    best = (-1.0, 1)
+    for b in (1, 2, 4, 8):
+        if b > n_sets or (recompute and b > 4):
+            break
+        p = make_bg_plan(N, j, setb=b, store=store, sp=sp)
+        wpb, blocks = choose_launch(p)
+        if wpb * 32 < p.G:
+            continue
+        util, _ = lane_utilisation(p)
+        score = util * min(16, wpb * blocks) / 16
+        if score > best[0] * 1.01:
+            best = (score, b)
+    return best[1]
 
 
 def default_bg_store(N: int, j: int) -> int:
@@ -108,9 +170,8 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     SP = sp if sp is not None else PITCH_BG.get(N, 10)
     if store is None:
         store = default_bg_store(N, j)
-    recompute = store + 1 < max(j, N - j)
     if setb is None:
-        setb = default_setb(N, j) if not recompute else min(4, default_setb_rec(N, j))
+        setb = default_setb(N, j, store, SP)
     lay: dict[str, int] = {}
     off = 0
 
@@ -202,7 +263,10 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
             t = [task("out", T, h, node_off("out", T, h), mask_off(full & ~msk(T)))
                  for T in _subsets(N, k) for h in range(1 << (k + 1))]
             plan.levels.append(("out", k, t))
-    for A in itertools.combinations(range(N), j):
+    subsets = list(itertools.combinations(range(N), j))
+    plan.n_sets_real = len(subsets)
+    subsets += [subsets[-1]] * (-len(subsets) % setb)   # ragged last batch: padding, joins skipped
+    for A in subsets:
         Ac = tuple(x for x in range(N) if x not in A)
         plan.sets.append(A)
         pos = [0] * N
@@ -251,7 +315,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     stored_rec = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"])
                      for k in range(store + 1, j)) + \
         sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(store + 1, N - j))
-    plan.recompute_flops = rec - stored_rec          # executed on top of the algorithmic count
+    n_pad = len(plan.sets) - plan.n_sets_real
+    pad_leaf = n_pad * ((1 << (j + 1)) * (vflops(j) + F["S"]) + (1 << (N - j + 1)) * vflops(N - j))
+    plan.recompute_flops = rec - stored_rec + pad_leaf   # executed on top of the algorithmic count
     plan.flops = {
         "external": N * F["EPS"] + 2 * F["SPINOR"],
         "propagator_constants": ((1 << N) - 2) * F["MASK"],

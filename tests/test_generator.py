@@ -150,9 +150,26 @@ def test_bg_recompute_and_large_tables_match_oracle(N, store):
 
 
 def test_bg_default_plans_n7_n8():
-    """n = 7, 8: levels above 2 recomputed per subset, two subsets per stage, fits one block's shared memory."""
-    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    """n = 7, 8: levels above 2 recomputed per subset, several subsets per stage, fits one block's
+    shared memory; the subset list is padded to whole batches (C(8,4) = 70, C(9,4) = 126)."""
+    import math
+    from paper_2511_19456_b200.gen.lower_bg import lane_utilisation, make_bg_plan
     for N in (8, 9):
         p = make_bg_plan(N)
-        assert p.store == 2 and p.dw == 16 and p.setb == 2
+        assert p.store == 2 and p.dw == 16 and p.setb >= 2
         assert p.stride * 8 < 227 * 1024
+        assert p.n_sets_real == math.comb(N, p.j) and len(p.sets) % p.setb == 0
+        assert len(p.sets) - p.n_sets_real < p.setb
+        assert all(A == p.sets[p.n_sets_real - 1] for A in p.sets[p.n_sets_real:])
+        assert lane_utilisation(p)[0] > 0.8
+
+
+def test_bg_lane_utilisation_model():
+    """The schedule model: one subset per stage leaves most lanes idle at n = 6 (16 + 32 leaf tasks on
+    128 lanes); the default batch recovers it; a perfectly packed stage has utilisation 1."""
+    from paper_2511_19456_b200.gen.lower_bg import lane_utilisation, make_bg_plan
+    u1, by1 = lane_utilisation(make_bg_plan(7, setb=1))
+    ud, _ = lane_utilisation(make_bg_plan(7))
+    assert by1["leaf"][1] / (128 * by1["leaf"][0]) < 0.4 and ud > u1 + 0.2
+    u2, _ = lane_utilisation(make_bg_plan(2))
+    assert u2 == 1.0
