@@ -86,6 +86,35 @@ __device__ __forceinline__ spinor eslash_row(const double* e, const spinor& p) {
   return o;
 }
 
+// transverse polarisation eps(k, 2) = (-sin phi, cos phi, 0): e3 = 0 is structural (SURVEY.md §8(c)
+// item 4), so its vertex drops the e3 terms: 8 real outputs x 2 ops            [V_T, 24 flop]
+__device__ __forceinline__ void emul_col_t(double e1, double e2, c2 x, c2 y, double sgn, c2& o0, c2& o1) {
+  double se1 = sgn * e1, se2 = sgn * e2;
+  o0.r = fma(se2, y.i, se1 * y.r);
+  o0.i = fma(-se2, y.r, se1 * y.i);
+  o1.r = fma(-se2, x.i, se1 * x.r);
+  o1.i = fma(se2, x.r, se1 * x.i);
+}
+__device__ __forceinline__ void emul_row_t(double e1, double e2, c2 x, c2 y, double sgn, c2& o0, c2& o1) {
+  double se1 = sgn * e1, se2 = sgn * e2;
+  o0.r = fma(-se2, y.i, se1 * y.r);
+  o0.i = fma(se2, y.r, se1 * y.i);
+  o1.r = fma(se2, x.i, se1 * x.r);
+  o1.i = fma(-se2, x.r, se1 * x.i);
+}
+__device__ __forceinline__ spinor eslash_col_t(const double* e, const spinor& p) {
+  spinor o;
+  emul_col_t(e[0], e[1], p.v[2], p.v[3], -1.0, o.v[0], o.v[1]);
+  emul_col_t(e[0], e[1], p.v[0], p.v[1], 1.0, o.v[2], o.v[3]);
+  return o;
+}
+__device__ __forceinline__ spinor eslash_row_t(const double* e, const spinor& p) {
+  spinor o;
+  emul_row_t(e[0], e[1], p.v[2], p.v[3], 1.0, o.v[0], o.v[1]);
+  emul_row_t(e[0], e[1], p.v[0], p.v[1], -1.0, o.v[2], o.v[3]);
+  return o;
+}
+
 // accumulating vertices (Berends-Giele currents): acc += epsslash psi / acc += psibar epsslash
 // (8 real outputs x 3 FMA = 48 flop)
 __device__ __forceinline__ void emul_col_acc(double e1, double e2, double e3, c2 x, c2 y, double sgn, c2& o0, c2& o1) {

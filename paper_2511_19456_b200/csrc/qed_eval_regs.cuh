@@ -88,6 +88,12 @@ __device__ __forceinline__ void ld_stream_eps(const double* p, double (&e)[3]) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e[0]), "=d"(e[1]) : "r"(addr));
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(e[2]) : "r"(addr + 16));
 }
+// transverse eps(k, 2): only (e1, e2) are loaded (e3 = 0 is structural)
+__device__ __forceinline__ void ld_stream_eps_t(const double* p, double (&e)[3]) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e[0]), "=d"(e[1]) : "r"(addr));
+  e[2] = 0.0;
+}
 __device__ __forceinline__ void ld_stream_mask(const double* p, double (&m)[5]) {
   const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(m[0]), "=d"(m[1]) : "r"(addr));

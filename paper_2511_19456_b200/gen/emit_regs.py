@@ -26,6 +26,8 @@ from .lower import FLOPS
 
 
 def _flops(N: int) -> dict:
+    """Flops per point of the emitted body.  Half of every vertex count has lam = 1, whose
+    polarisation eps(k, 2) is transverse (eps^3 = 0): V_T = 24 instead of V = 40."""
     H = 1 << (N + 2)
     n_phi = N * 4                                   # leaves phi_a[s][lam]
     if N == 2:
@@ -34,11 +36,12 @@ def _flops(N: int) -> dict:
         n_int = N * 2 * 2                           # ubar eps_b S, both s'
         n_leaf = N * (N - 1) * 4 * 2                # (b, c) x lam_b lam_c x s'
     import math
+    V2 = FLOPS["V"] + FLOPS["V_T"]                  # one vertex of each polarisation
     return {
         "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
         "propagator_constants": (N + (N if N > 2 else 0)) * FLOPS["MASK"],
-        "trie_in": n_phi * (FLOPS["V"] + FLOPS["S"]),
-        "trie_out": n_int * (FLOPS["V"] + FLOPS["S"]) + n_leaf * FLOPS["V"],
+        "trie_in": n_phi // 2 * V2 + n_phi * FLOPS["S"],
+        "trie_out": n_int // 2 * V2 + n_int * FLOPS["S"] + n_leaf // 2 * V2,
         "join": math.factorial(N) * H * FLOPS["JOIN"],
         "msq": H * FLOPS["ABS2"],
     }
@@ -57,6 +60,9 @@ def slot_layout(N: int) -> dict:
         off += 2                      # odd number of 16-byte slots per point (bank spread)
     lay["STRIDE"] = off
     return lay
+
+
+T_ = ("", "_t")   # vertex of polarisation lam: eps(k, 2) (lam = 1) is transverse, eps^3 = 0
 
 
 def emit_regs_body(N: int) -> str:
@@ -103,7 +109,7 @@ def emit_regs_body(N: int) -> str:
     for i in range(N):
         for lam in range(2):
             w(f"  qed::st_spinor(sl + (({i} * 2 + sp) * 2 + {lam}) * 8, qed::prop_col(sl + {lay['MASK'] + 6 * i}, "
-              f"qed::eslash_col(sl + {lay['EPS'] + 8 * i + 4 * lam}, u)));")
+              f"qed::eslash_col{T_[lam]}(sl + {lay['EPS'] + 8 * i + 4 * lam}, u)));")
     w("  __syncwarp();")
     w("  // out-side trie, depth first; joins against phi of the remaining photon")
     for b in range(N):
@@ -112,8 +118,8 @@ def emit_regs_body(N: int) -> str:
             if N == 2:
                 a_ = 1 - b
                 w(f"  {{  // tau = ({b}), lam_{b} = {lb}, remaining photon {a_}")
-                w(f"    double eb[3]; qed::ld_stream_eps(sl + {e_b}, eb);")
-                w(f"    const qed::spinor leaf = qed::eslash_row(eb, ub);")
+                w(f"    double eb[3]; qed::ld_stream_eps{T_[lb]}(sl + {e_b}, eb);")
+                w(f"    const qed::spinor leaf = qed::eslash_row{T_[lb]}(eb, ub);")
                 w("    #pragma unroll")
                 w("    for (int k = 0; k < 4; ++k) {")
                 w(f"      const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
@@ -124,17 +130,17 @@ def emit_regs_body(N: int) -> str:
             else:
                 w(f"  {{  // tau_1 = photon {b}, lam_{b} = {lb}")
                 w("    __syncwarp();")
-                w(f"    double eb[3], mb[5]; qed::ld_stream_eps(sl + {e_b}, eb); qed::ld_stream_mask(sl + {lay['MASK'] + 6 * (N + b)}, mb);")
-                w(f"    const qed::spinor I = qed::prop_row(mb, qed::eslash_row(eb, ub));")
+                w(f"    double eb[3], mb[5]; qed::ld_stream_eps{T_[lb]}(sl + {e_b}, eb); qed::ld_stream_mask(sl + {lay['MASK'] + 6 * (N + b)}, mb);")
+                w(f"    const qed::spinor I = qed::prop_row(mb, qed::eslash_row{T_[lb]}(eb, ub));")
                 for c in range(N):
                     if c == b:
                         continue
                     a_ = 3 - b - c
                     w(f"    {{  // tau_2 = photon {c}, remaining photon {a_}")
                     w("      __syncwarp();  // scheduling fence: ptxas would otherwise hoist every phi load and spill")
-                    w(f"      double ec0[3], ec1[3]; qed::ld_stream_eps(sl + {lay['EPS'] + 8 * c}, ec0); qed::ld_stream_eps(sl + {lay['EPS'] + 8 * c + 4}, ec1);")
+                    w(f"      double ec0[3], ec1[3]; qed::ld_stream_eps(sl + {lay['EPS'] + 8 * c}, ec0); qed::ld_stream_eps_t(sl + {lay['EPS'] + 8 * c + 4}, ec1);")
                     w(f"      const qed::spinor l0 = qed::eslash_row(ec0, I);")
-                    w(f"      const qed::spinor l1 = qed::eslash_row(ec1, I);")
+                    w(f"      const qed::spinor l1 = qed::eslash_row_t(ec1, I);")
                     w("      #pragma unroll")
                     w("      for (int k = 0; k < 4; ++k) {")
                     w(f"        const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")

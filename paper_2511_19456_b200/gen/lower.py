@@ -44,6 +44,7 @@ from .dag import balanced_split, perm_count
 # flop model of the emitted device code (FMA = 2, add/mul = 1; csrc/qed_device.cuh)
 FLOPS = {
     "V": 40,          # epsslash psi: 8 real outputs x (1 mul + 2 fma)
+    "V_T": 24,        # the same for the transverse eps(k, 2) (eps^3 = 0): 8 x (1 mul + 1 fma); regs kernels
     "S": 56,          # (Qslash+m)/D psi with pre-scaled constants: 8 x (1 mul + 3 fma)
     "JOIN": 32,       # 4 complex multiply-accumulates
     "ABS2": 4,        # |amp|^2 accumulated: fma + fma
