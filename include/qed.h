@@ -77,7 +77,8 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
    exponential scaling: the sum over the
    orderings of each photon subset is taken inside the propagators (Berends-Giele currents), one join
    per subset.  Same |M|^2 (same oracle), fewer flops: 7.8 k vs 10.7 k (n = 2), 310 k vs 6.2 M (n = 5).
-   variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable. */
+   variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable; an index
+   >= qed_process_info.n_variants is QED_ERR_INVALID_ARGUMENT. */
 typedef enum { QED_ALGO_CDAG = 0, QED_ALGO_BERENDS_GIELE = 1 } qed_algorithm;
 typedef struct {
   int algorithm;
@@ -148,6 +149,7 @@ typedef struct {
   int64_t bytes_per_point;   /* algorithmic HBM bytes per point (momenta in + |M|^2 out) */
   int algorithm;             /* qed_algorithm */
   int variant;               /* launch variant in use */
+  int n_variants;            /* launch variants compiled for this size and algorithm (0 .. n_variants-1) */
 } qed_process_info;
 qed_status qed_get_process_info(const qed_process* proc, qed_process_info* info);
 

@@ -132,7 +132,7 @@ struct qed_process {
   qed::QedEvalArgs args{};
   const void* kern[2] = {nullptr, nullptr};
   const void* kern_mc = nullptr;
-  int variant = 0, algorithm = 0;
+  int variant = 0, n_variants = 1, algorithm = 0;
   int wpb = 0, ppw = 0, grid_blocks = 0, mc_wpb = 0, mc_grid_blocks = 0, device = 0, num_sms = 0;
   long long smem = 0, smem_mc = 0, flops = 0;
   // staging for the host-buffer entry point
@@ -236,15 +236,25 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   const bool use_regs = algorithm == QED_ALGO_CDAG && N <= 3 && !(force && strcmp(force, "group") == 0);
   if (use_regs) {
     const int nv = N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3();
-    const int v = (options && options->variant >= 0 && options->variant < nv) ? options->variant : variant_from_env(nv);
+    if (options && options->variant >= nv) {
+      delete P;
+      return fail(QED_ERR_INVALID_ARGUMENT, "options.variant " + std::to_string(options->variant) + " >= " + std::to_string(nv));
+    }
+    const int v = (options && options->variant >= 0) ? options->variant : variant_from_env(nv);
     P->variant = v;
+    P->n_variants = nv;
     P->kern[0] = N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
     P->kern[1] = N == 2 ? qedregs_kernel_N2(1, v) : qedregs_kernel_N3(1, v);
     (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
   } else {
     const int nv = ke.num_variants();
-    const int v = (options && options->variant >= 0 && options->variant < nv) ? options->variant : variant_from_env(nv);
+    if (options && options->variant >= nv) {
+      delete P;
+      return fail(QED_ERR_INVALID_ARGUMENT, "options.variant " + std::to_string(options->variant) + " >= " + std::to_string(nv));
+    }
+    const int v = (options && options->variant >= 0) ? options->variant : variant_from_env(nv);
     P->variant = v;
+    P->n_variants = nv;
     P->kern[0] = ke.kernel(0, v);
     P->kern[1] = ke.kernel(1, v);
     ke.config(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
@@ -402,6 +412,7 @@ qed_status qed_get_process_info(const qed_process* P, qed_process_info* info) {
   info->bytes_per_point = 8LL * (4 * P->n_ext + 1);
   info->algorithm = P->algorithm;
   info->variant = P->variant;
+  info->n_variants = P->n_variants;
   return QED_OK;
 }
 

@@ -369,8 +369,9 @@ def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
     """Launch variants (body, warps per block, min resident blocks, L2 prefetch); QED_VARIANT selects.
     Variant 0 = best of the latest sweep (profiles/sweep_*.jsonl)."""
     if N == 3:
-        return [("T", 4, 1, 2), ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2),
-                ("TI", 4, 1, 2), ("TI", 4, 1, 1), ("T", 2, 5, 1), ("T", 2, 5, 0)]
+        # r20 sweep: the interleaved join body TI >= T at n = 2 once the transverse vertices shortened T
+        return [("TI", 4, 1, 2), ("T", 4, 1, 2), ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1),
+                ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
     return [("T", 2, 6, 2), ("T", 4, 1, 0), ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
 
 

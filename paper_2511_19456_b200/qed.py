@@ -50,7 +50,7 @@ class ProcessInfo(ctypes.Structure):
                 ("n_diagrams", ctypes.c_int), ("lanes_per_point", ctypes.c_int), ("warps_per_block", ctypes.c_int),
                 ("smem_per_block", ctypes.c_int64), ("grid_blocks", ctypes.c_int),
                 ("flops_per_point", ctypes.c_int64), ("bytes_per_point", ctypes.c_int64),
-                ("algorithm", ctypes.c_int), ("variant", ctypes.c_int)]
+                ("algorithm", ctypes.c_int), ("variant", ctypes.c_int), ("n_variants", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

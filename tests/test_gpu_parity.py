@@ -323,3 +323,29 @@ def test_bg_large_n_invariances(qed, n):
     assert np.all(np.isfinite(a)) and np.all(a > 0)
     assert np.max(np.abs(b / a - 1)) <= 1e-9
     assert np.max(np.abs(c / a - 1)) <= TOL      # rounding order changes with the permutation
+
+
+# every compiled launch variant (QED_VARIANT / qed_process_options.variant), averaged and per
+# configuration: non-default variants are what the tuning sweeps time, so they are held to parity too
+VARIANT_CASES = [("cdag", n) for n in (1, 2, 3, 4, 5)] + [("bg", n) for n in (1, 2, 3, 4, 5, 6)]
+
+
+@pytest.mark.parametrize("algorithm,n", VARIANT_CASES)
+def test_every_launch_variant_matches_oracle(qed, algorithm, n):
+    npts = {1: 1029, 2: 1029, 3: 517, 4: 131, 5: 37, 6: 9}[n]
+    mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=3100 + n)
+    ref = oracle.msq(1, n, mom.numpy())
+    A = oracle.amps(1, n, mom[:5].numpy())
+    ref_cfg = np.abs(A) ** 2
+    nv = qed.Process(n, algorithm=algorithm).info()["n_variants"]
+    assert nv >= 1
+    for v in range(nv):
+        proc = qed.Process(n, algorithm=algorithm, variant=v)
+        assert proc.info()["variant"] == v
+        got = _gpu_msq(qed, proc, mom)
+        rel = np.abs(got / ref - 1)
+        assert rel.max() <= TOL, (v, rel.max())
+        cfg = _gpu_configs(qed, proc, mom[:5])
+        assert (np.abs(cfg - ref_cfg) / ref_cfg.max(axis=1, keepdims=True)).max() <= TOL, v
+    with pytest.raises(qed.QedError):
+        qed.Process(n, algorithm=algorithm, variant=nv)
