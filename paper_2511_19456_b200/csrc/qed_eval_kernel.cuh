@@ -283,13 +283,80 @@ __device__ __forceinline__ void join_set(const double* __restrict__ base, unsign
   }
 }
 
+// Two-half joins (T::HS == 2, gen/lower.py hs_table; Berends-Giele plans, NSIG = NTAU = 1): lane g' of
+// either half owns the 8 configurations (s, s', lam_x), x = N - 1, in acc[2 k], k = s | s' << 1 |
+// lam_x << 2.  XIN (x in A): 4 phi (lam_x, s) x 2 ubar (s'); else 2 phi (s) x 4 ubar (lam_x, s').
+// 6 spinor loads per 8 joins instead of 4 per 4: the join's shared-memory traffic drops by a quarter.
+template <class T, bool XIN>
+__device__ __forceinline__ void join_set_hs(const double* __restrict__ base, uint2 w, double (&acc)[16], int lb) {
+  static_assert(T::NSIG == 1 && T::NTAU == 1, "two-half joins: one phi and one ubar row per subset");
+  constexpr int NP = XIN ? 4 : 2, NU = XIN ? 2 : 4;
+  base += lb * T::LEAFB;
+  int po[NP], uo[NU];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) po[i] = (w.x >> (8 * i)) & 255;
+#pragma unroll
+  for (int i = 0; i < NU; ++i) uo[i] = (w.y >> (8 * i)) & 255;
+  const double* prow = base + T::PHI;
+  const double* urow = base + T::UBL;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    c2 p[NP], u[NU];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) p[i] = ld2(prow + c * T::NHI * 2 + po[i]);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = ld2(urow + c * T::NHO * 2 + uo[i]);
+#pragma unroll
+    for (int ip = 0; ip < NP; ++ip)
+#pragma unroll
+      for (int iu = 0; iu < NU; ++iu) {
+        const int k = XIN ? ((ip & 1) | (iu << 1) | ((ip >> 1) << 2)) : (ip | ((iu & 1) << 1) | ((iu >> 1) << 2));
+        acc[2 * k] = fma(u[iu].r, p[ip].r, fma(-u[iu].i, p[ip].i, acc[2 * k]));
+        acc[2 * k + 1] = fma(u[iu].r, p[ip].i, fma(u[iu].i, p[ip].r, acc[2 * k + 1]));
+      }
+  }
+}
+
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
 template <class T, int AS = 2>
-__device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[8]) {
+__device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
   T::run_interiors(base, g, pb);
+  if constexpr (T::HS == 2) {
+    // half q joins subsets s0 + q, s0 + q + 2, ... of every batch; the halves' partial amplitudes are
+    // summed into half 0 at the end through shared memory (the dead U.. region of the point's slot)
+    constexpr int GH = T::G / 2;
+    const int q = g / GH, gh = g % GH;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
+      T::run_set(base, g, pb, s0);
+      group_sync<T>(pb);
+#pragma unroll
+      for (int lb = 0; lb < T::SETB; lb += 2) {
+        const int si = s0 + lb + q;
+        if (T::NSETS_REAL % T::SETB == 0 || si < T::NSETS_REAL) {
+          const uint2 w = T::hs_offsets(si, gh);
+          if ((T::set_mask(si) >> (T::N - 1)) & 1) join_set_hs<T, true>(base, w, acc, lb + q);
+          else join_set_hs<T, false>(base, w, acc, lb + q);
+        }
+      }
+      group_sync<T>(pb);
+    }
+    double* red = base + T::U;
+    if (q == 1) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) red[i * GH + gh] = acc[i];
+    }
+    group_sync<T>(pb);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) amp[i] = q == 0 ? acc[i] + red[i * GH + gh] : 0.0;
+    return;
+  } else {
   double acc[AS][8];   // AS independent partial sums per amplitude (ILP across the c loop)
 #pragma unroll
   for (int q = 0; q < AS; ++q)
@@ -311,21 +378,29 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     for (int q = 1; q < AS; ++q) s += acc[q][i];
     amp[i] = s;
   }
+  }
 }
 
-// internal configuration of amplitude k of lane g: s | lam << 1 | s' << (N+1)
+// internal configuration of amplitude k of lane g: s | lam << 1 | s' << (N+1); with two-half joins
+// lane g' = g mod G/2 holds lam_0..lam_{N-2} and k = s | s' << 1 | lam_{N-1} << 2 (half 0 only)
 template <class T>
 __device__ __forceinline__ unsigned config_of(int k, int g) {
+  if constexpr (T::HS == 2) {
+    const unsigned gh = g % (T::G / 2);
+    return (k & 1) | (gh << 1) | ((unsigned)((k >> 2) & 1) << T::N) | ((unsigned)((k >> 1) & 1) << (T::N + 1));
+  }
   return (k & 1) | ((unsigned)g << 1) | ((unsigned)(k >> 1) << (T::N + 1));
 }
+template <class T>
+__device__ __forceinline__ bool holds_amps(int g) { return T::HS == 1 || g < T::G / 2; }
 
 // sum over the group's configurations allowed by the spec of |amp|^2, times norm (valid in every
 // lane of groups of <= 32 lanes, and in every lane of 64-lane groups after the barrier exchange)
 template <class T>
-__device__ __forceinline__ double group_msq(const double (&amp)[8], int g, int pb, double* base, const QedEvalArgs& a) {
+__device__ __forceinline__ double group_msq(const double (&amp)[2 * T::NAMP], int g, int pb, double* base, const QedEvalArgs& a) {
   double sum = 0.0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < T::NAMP; ++k) {
     const double t = fma(amp[2 * k], amp[2 * k], amp[2 * k + 1] * amp[2 * k + 1]);
     sum += ((config_of<T>(k, g) & a.fixed_mask) == a.fixed_val) ? t : 0.0;
   }
@@ -364,13 +439,13 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
       if (V::PF && pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
     }
     group_sync<T>(pb);
-    double amp[8];
+    double amp[2 * T::NAMP];
     eval_point<T, V::AS>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
-      if (valid) {
+      if (valid && holds_amps<T>(g)) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < T::NAMP; ++k) {
           const unsigned h = config_of<T>(k, g);
           unsigned hx = 0;
 #pragma unroll

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
         for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
       }
       group_sync<T>(pb);
-      double amp[8];
+      double amp[2 * T::NAMP];
       eval_point<T, V::AS>(base, g, pb, a, amp);
       const double msq = group_msq<T>(amp, g, pb, base, a);
       if (g == 0) {

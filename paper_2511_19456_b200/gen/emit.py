@@ -121,6 +121,7 @@ struct T {{
   static constexpr int {lay};
   static constexpr int NSIG = {plan.n_sigma}, NTAU = {plan.n_tau}, NHI = {plan.n_hi}, NHO = {plan.n_ho};
   static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = NSETS, SETB = 1, LEAFB = 0;
+  static constexpr int HS = 1, NAMP = 4;
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}

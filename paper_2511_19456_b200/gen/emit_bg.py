@@ -10,7 +10,7 @@ from __future__ import annotations
 import os
 
 from .emit import choose_launch, lane_offset
-from .lower import hiho_table
+from .lower import hiho_table, hs_table
 from .lower_bg import BGPlan, make_bg_plan
 
 
@@ -89,6 +89,7 @@ def emit_bg_source(plan: BGPlan) -> str:
     set_pos = [p for ps in plan.set_pos for p in ps]
     set_mask = [sum(1 << x for x in A) for A in plan.sets]
     hiho = hiho_table(plan)
+    hst = hs_table(plan) if plan.hs == 2 else [0, 0]
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in plan.flops.items())
     lay = ", ".join(f"{k} = {L[k]}" for k in ("MOM", "RED", "EPS", "MASK", "U", "UB", "PHI", "UBL"))
     variant_structs = "".join(f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }};\n"
@@ -117,6 +118,8 @@ __device__ const unsigned char k_set_pos[{len(set_pos)}] = {{{", ".join(map(str,
 __device__ const unsigned k_set_mask[{len(set_mask)}] = {{{", ".join(map(str, set_mask))}}};
 // per (subset, lane): packed 2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1) (leaf-row offsets of the lane's tile)
 __device__ const unsigned k_hiho[{len(hiho)}] = {{{", ".join(f"0x{x:08x}u" for x in hiho)}}};
+// two-half joins (hs = {plan.hs}): per (subset, lane of a half) phi / ubar offsets of the (s, s', lam_x) tile
+__device__ const uint2 k_hs[{max(1, len(hst) // 2)}] = {{{", ".join(f"{{0x{hst[i]:08x}u, 0x{hst[i + 1]:08x}u}}" for i in range(0, len(hst), 2))}}};
 
 struct T {{
   static constexpr int N = {N}, J = {plan.j}, G = {plan.G}, DW = {plan.dw};
@@ -124,10 +127,12 @@ struct T {{
   static constexpr int {lay};
   static constexpr int NSIG = 1, NTAU = 1, NHI = {plan.n_hi}, NHO = {plan.n_ho};
   static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = {plan.n_sets_real}, SETB = {B}, LEAFB = {L['LEAFB']};
+  static constexpr int HS = {plan.hs}, NAMP = 4 * HS;   // join halves, amplitudes per lane
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
   static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
+  static __device__ __forceinline__ uint2 hs_offsets(int si, int gh) {{ return __ldg(k_hs + si * (G / 2) + gh); }}
   static __device__ __forceinline__ void run_interiors(double* base, int g, int pb) {{
 {interiors}
   }}

@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from .lower import Plan, aos_slot, hiho_table
+from .lower import Plan, aos_slot, hiho_table, hs_table
 
 ALPHA = 1 / 137.035999084
 
@@ -54,6 +54,18 @@ def _join_offsets(hiho, si, G, h, N):
     w = hiho[si * G + ((h >> 1) & (G - 1))]
     s, sp = h & 1, (h >> (N + 1)) & 1
     return (w >> (8 * s)) & 255, (w >> (16 + 8 * sp)) & 255
+
+
+def _join_offsets_hs(tab, plan, si, h):
+    """The same offsets from the two-half table (lower.hs_table): lane g' = lam_0..lam_{N-2}, tile
+    (s, s', lam_x), x = N - 1."""
+    N, x = plan.N, plan.N - 1
+    gp = (h >> 1) & ((1 << x) - 1)
+    s, sp, lx = h & 1, (h >> (N + 1)) & 1, (h >> (1 + x)) & 1
+    wp, wu = tab[2 * (si * (plan.G // 2) + gp)], tab[2 * (si * (plan.G // 2) + gp) + 1]
+    if x in plan.sets[si]:
+        return (wp >> (8 * (2 * lx + s))) & 255, (wu >> (8 * sp)) & 255
+    return (wp >> (8 * s)) & 255, (wu >> (8 * (2 * lx + sp))) & 255
 
 
 def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
@@ -172,6 +184,7 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
             sm[o], sm[o + 1] = v[c].real, v[c].imag
 
     hiho = hiho_table(plan)
+    hst = hs_table(plan) if getattr(plan, "hs", 1) == 2 else None
 
     def get_leaf_off(base, nh, o2, lb=0):
         o = base + lb * LB + o2
@@ -239,7 +252,10 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         if si >= plan.n_sets_real:      # padding subset of a ragged last batch
             continue
         for h in range(H):
-            oi, oo = _join_offsets(hiho, si, plan.G, h, N)
+            if hst is not None:
+                oi, oo = _join_offsets_hs(hst, plan, si, h)
+            else:
+                oi, oo = _join_offsets(hiho, si, plan.G, h, N)
             amp[h] += get_leaf_off(L["UBL"], plan.n_ho, oo, lb) @ get_leaf_off(L["PHI"], plan.n_hi, oi, lb)
     e_n = math.sqrt(4 * math.pi * ALPHA) ** N
     out = np.zeros(H, dtype=complex)

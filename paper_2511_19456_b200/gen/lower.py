@@ -358,3 +358,34 @@ def hiho_table(plan) -> list[int]:
             assert max(w) < 256
             out.append(w[0] | w[1] << 8 | w[2] << 16 | w[3] << 24)
     return out
+
+
+def hs_table(plan) -> list[int]:
+    """Two-half join tables (plan.hs == 2).  The last photon x = N - 1 leaves the lane index: lane
+    g' < G/2 of either half owns the 8 configurations (s, s', lam_x) x (lam_i = bit i of g', i < x).
+    Per (subset si, g') two words of four byte offsets (2 swz(h), leaf rows as in hiho_table):
+      x in A:  phi for (lam_x, s) = (0,0) (0,1) (1,0) (1,1), ubar for s' = 0, 1 (bytes 2, 3 zero)
+      x in Ac: phi for s = 0, 1 (bytes 2, 3 zero), ubar for (lam_x, s') = (0,0) (0,1) (1,0) (1,1)
+    Flattened as [si][g'][word]."""
+    N, x = plan.N, plan.N - 1
+    out = []
+    for si, A in enumerate(plan.sets):
+        pos = plan.set_pos[si]
+        for gp in range(plan.G // 2):
+            hi = ho = 0
+            for i in range(x):
+                lam = (gp >> i) & 1
+                if i in A:
+                    hi |= lam << pos[i]
+                else:
+                    ho |= lam << pos[i]
+            if x in A:
+                ph = [2 * swz(s | hi | (lx << pos[x])) for lx in (0, 1) for s in (0, 1)]
+                ub = [2 * swz(sp | ho) for sp in (0, 1)] + [0, 0]
+            else:
+                ph = [2 * swz(s | hi) for s in (0, 1)] + [0, 0]
+                ub = [2 * swz(sp | ho | (lx << pos[x])) for lx in (0, 1) for sp in (0, 1)]
+            assert max(ph + ub) < 256
+            out.append(ph[0] | ph[1] << 8 | ph[2] << 16 | ph[3] << 24)
+            out.append(ub[0] | ub[1] << 8 | ub[2] << 16 | ub[3] << 24)
+    return out

@@ -48,6 +48,7 @@ class BGPlan:
     set_pos: list[list[int]] = field(default_factory=list)
     flops: dict[str, int] = field(default_factory=dict)
     n_sets_real: int = 0     # C(N, j); sets[n_sets_real:] pad the last batch to SETB subsets
+    hs: int = 1              # join halves (lower.hs_table): 1 = lane tile (s, s'); 2 = (s, s', lam_{N-1})
 
     @property
     def H(self) -> int:
@@ -160,8 +161,14 @@ def default_bg_store(N: int, j: int) -> int:
     return N if spinors(N) * 64 <= 110 * 1024 else 2
 
 
+def default_hs(N: int) -> int:
+    """Join halves where they measured faster (profiles/sweep_r21.jsonl vs sweep_r18: n = 6 +6 %,
+    n = 8 +11 %; n = 4 -5 %, n = 5 flat, n = 7 -1.5 %)."""
+    return 2 if N in (7, 9) else 1
+
+
 def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None,
-                 sp: int | None = None) -> BGPlan:
+                 sp: int | None = None, hs: int | None = None) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
@@ -170,8 +177,12 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     SP = sp if sp is not None else PITCH_BG.get(N, 10)
     if store is None:
         store = default_bg_store(N, j)
+    if hs is None:
+        hs = default_hs(N)
     if setb is None:
         setb = default_setb(N, j, store, SP)
+    if hs == 2 and setb % 2:
+        setb *= 2                                   # one subset per half and batch at least
     lay: dict[str, int] = {}
     off = 0
 
@@ -214,6 +225,8 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     if (stride // 2) % 2 == 0:
         stride += 2
     lay["STRIDE"] = stride
+    if hs == 2:    # the halves' amplitude reduction reuses the slot from U on (dead after the last join)
+        assert lay["U"] + 16 * (G // 2) <= stride, (N, lay["U"], stride)
 
     def eps_off(i, lam):
         return lay["EPS"] + (i * 2 + lam) * 4
@@ -264,6 +277,11 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
                  for T in _subsets(N, k) for h in range(1 << (k + 1))]
             plan.levels.append(("out", k, t))
     subsets = list(itertools.combinations(range(N), j))
+    if hs == 2:
+        # two-half joins (lower.hs_table): subsets containing photon N-1 first, so that the two halves
+        # of a batch take the same join shape (at most one mixed pair)
+        subsets = [A for A in subsets if N - 1 in A] + [A for A in subsets if N - 1 not in A]
+    plan.hs = hs
     plan.n_sets_real = len(subsets)
     subsets += [subsets[-1]] * (-len(subsets) % setb)   # ragged last batch: padding, joins skipped
     for A in subsets:

@@ -168,8 +168,24 @@ def test_bg_lane_utilisation_model():
     """The schedule model: one subset per stage leaves most lanes idle at n = 6 (16 + 32 leaf tasks on
     128 lanes); the default batch recovers it; a perfectly packed stage has utilisation 1."""
     from paper_2511_19456_b200.gen.lower_bg import lane_utilisation, make_bg_plan
-    u1, by1 = lane_utilisation(make_bg_plan(7, setb=1))
+    u1, by1 = lane_utilisation(make_bg_plan(7, setb=1, hs=1))
     ud, _ = lane_utilisation(make_bg_plan(7))
     assert by1["leaf"][1] / (128 * by1["leaf"][0]) < 0.4 and ud > u1 + 0.2
     u2, _ = lane_utilisation(make_bg_plan(2))
     assert u2 == 1.0
+
+
+@pytest.mark.parametrize("N,hs", [(4, 2), (5, 2), (6, 2), (5, 1), (7, 1)])
+def test_bg_join_halves_match_oracle(N, hs):
+    """Two-half joins (lower.hs_table: lane tile (s, s', lam_{N-1}), subsets split over the halves of
+    the group) and the one-tile form, each against the oracle through the interpreter."""
+    from paper_2511_19456_b200.gen.interp import eval_point_bg
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    n = N - 1
+    plan = make_bg_plan(N, hs=hs)
+    assert plan.hs == hs and (hs == 1 or plan.setb % 2 == 0)
+    mom = synthetic.rambo_cm(n, 2, sqrt_s=5.0, seed=700 + n).numpy()
+    A = oracle.amps(1, n, mom)
+    for k in range(2):
+        B = eval_point_bg(plan, mom[k], 1)
+        assert np.max(np.abs(A[k] - B)) <= 1e-12 * np.max(np.abs(A[k]))
