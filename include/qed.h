@@ -104,9 +104,11 @@ qed_status qed_eval_msq(const qed_process* proc, const double* momenta, int64_t 
 qed_status qed_eval_msq_configs(const qed_process* proc, const double* momenta, int64_t n_points,
                                 double* out, void* stream);
 
-/* Same as qed_eval_msq, but momenta and out are HOST buffers: copies them through
-   device staging buffers owned by the handle and returns after the result is on
-   the host (end-to-end path).  Synchronous. */
+/* Same as qed_eval_msq, but momenta and out are HOST buffers (same layouts; pin them with
+   cudaHostAlloc / cudaHostRegister for full PCIe bandwidth): copies them through two chunk staging
+   buffers owned by the handle, pipelined over chunks of >= 2^18 points on two streams owned by the
+   handle (upload of chunk c+1 overlaps kernel and download of chunk c), and returns after the result
+   is on the host (end-to-end path).  Synchronous; calls on one handle are serialised. */
 qed_status qed_eval_msq_host(const qed_process* proc, const double* momenta_host, int64_t n_points,
                              double* out_host);
 

@@ -127,6 +127,8 @@ int variant_from_env(int n_variants) {
 
 }  // namespace
 
+constexpr long long kHostChunkMin = 1LL << 18;   // points per pipelined chunk of qed_eval_msq_host (minimum)
+
 struct qed_process {
   int n = 0, N = 0, n_in_ph = 0, n_out_ph = 0, n_ext = 0;
   qed::QedEvalArgs args{};
@@ -137,10 +139,11 @@ struct qed_process {
   long long smem = 0, smem_mc = 0, flops = 0;
   // staging for the host-buffer entry point
   std::mutex mu;
-  double* d_mom = nullptr;
-  double* d_out = nullptr;
+  // host entry point: two chunk staging buffers (momenta SoA of kHostChunk points, out), one stream each
+  double* d_mom[2] = {nullptr, nullptr};
+  double* d_out[2] = {nullptr, nullptr};
   long long cap = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t hstream[2] = {nullptr, nullptr};
 };
 
 extern "C" {
@@ -293,9 +296,11 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
 
 qed_status qed_process_destroy(qed_process* proc) {
   if (!proc) return QED_OK;
-  if (proc->d_mom) cudaFree(proc->d_mom);
-  if (proc->d_out) cudaFree(proc->d_out);
-  if (proc->stream) cudaStreamDestroy(proc->stream);
+  for (int b = 0; b < 2; ++b) {
+    if (proc->d_mom[b]) cudaFree(proc->d_mom[b]);
+    if (proc->d_out[b]) cudaFree(proc->d_out[b]);
+    if (proc->hstream[b]) cudaStreamDestroy(proc->hstream[b]);
+  }
   delete proc;
   return QED_OK;
 }
@@ -339,30 +344,48 @@ qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_hos
   if (!momenta_host || !out_host) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
   std::lock_guard<std::mutex> lock(P->mu);
   cudaError_t e;
-  if (!P->stream) {
-    e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-  }
-  if (P->cap < n_points) {
-    if (P->d_mom) cudaFree(P->d_mom);
-    if (P->d_out) cudaFree(P->d_out);
-    P->d_mom = P->d_out = nullptr;
+  // Pipelined over chunks of points on two streams: chunk c's H2D (a 2D copy of its columns of the
+  // SoA rows), kernel and D2H go to stream c % 2 and its staging buffer, so the upload of chunk c+1
+  // overlaps the kernel and download of chunk c.  PCIe bound: ~160 B in per point at n = 2.
+  const long long chunk = std::min<long long>(n_points, std::max<long long>(kHostChunkMin, (n_points + 7) / 8));
+  for (int b = 0; b < 2; ++b)
+    if (!P->hstream[b]) {
+      e = cudaStreamCreateWithFlags(&P->hstream[b], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    }
+  if (P->cap < chunk) {
+    for (int b = 0; b < 2; ++b) {
+      if (P->d_mom[b]) cudaFree(P->d_mom[b]);
+      if (P->d_out[b]) cudaFree(P->d_out[b]);
+      P->d_mom[b] = P->d_out[b] = nullptr;
+    }
     P->cap = 0;
-    e = cudaMalloc(&P->d_mom, sizeof(double) * 4 * P->n_ext * (size_t)n_points);
-    if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging momenta");
-    e = cudaMalloc(&P->d_out, sizeof(double) * (size_t)n_points);
-    if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging out");
-    P->cap = n_points;
+    for (int b = 0; b < 2; ++b) {
+      e = cudaMalloc(&P->d_mom[b], sizeof(double) * 4 * P->n_ext * (size_t)chunk);
+      if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging momenta");
+      e = cudaMalloc(&P->d_out[b], sizeof(double) * (size_t)chunk);
+      if (e != cudaSuccess) return fail(QED_ERR_OUT_OF_MEMORY, "cudaMalloc staging out");
+    }
+    P->cap = chunk;
   }
-  e = cudaMemcpyAsync(P->d_mom, momenta_host, sizeof(double) * 4 * P->n_ext * (size_t)n_points,
-                      cudaMemcpyHostToDevice, P->stream);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-  qed_status st = launch_eval(P, P->d_mom, n_points, P->d_out, P->stream, 0);
-  if (st != QED_OK) return st;
-  e = cudaMemcpyAsync(out_host, P->d_out, sizeof(double) * (size_t)n_points, cudaMemcpyDeviceToHost, P->stream);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
-  e = cudaStreamSynchronize(P->stream);
-  if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  const int rows = 4 * P->n_ext;
+  int c = 0;
+  for (long long i0 = 0; i0 < n_points; i0 += chunk, ++c) {
+    const int b = c & 1;
+    const long long cnt = std::min<long long>(chunk, n_points - i0);
+    cudaStream_t st = P->hstream[b];
+    e = cudaMemcpy2DAsync(P->d_mom[b], sizeof(double) * (size_t)cnt, momenta_host + i0, sizeof(double) * (size_t)n_points,
+                          sizeof(double) * (size_t)cnt, rows, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    qed_status stt = launch_eval(P, P->d_mom[b], cnt, P->d_out[b], st, 0);
+    if (stt != QED_OK) return stt;
+    e = cudaMemcpyAsync(out_host + i0, P->d_out[b], sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  for (int b = 0; b < 2; ++b) {
+    e = cudaStreamSynchronize(P->hstream[b]);
+    if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  }
   return QED_OK;
 }
 

@@ -174,6 +174,29 @@ def test_host_entry_point(qed):
     assert np.max(np.abs(out.numpy() / ref - 1)) <= TOL
 
 
+def test_host_entry_point_pipelined_chunks(qed):
+    """qed_eval_msq_host over several pipelined chunks (>= 2^18 points each, two streams, ragged last
+    chunk): bitwise equal to the device entry point on the same points, oracle on samples around the
+    chunk boundaries; pageable (unpinned) host buffers work too."""
+    n, P = 1, 2 * (1 << 18) + 12345
+    mom = synthetic.rambo_cm(n, P, seed=8100)
+    soa = synthetic.to_soa(mom)
+    proc = qed.Process(n)
+    dev = torch.empty(P, dtype=torch.float64, device="cuda")
+    proc.eval_msq(soa.cuda(), dev)
+    torch.cuda.synchronize()
+    out = torch.full((P,), float("nan"), dtype=torch.float64).pin_memory()
+    proc.eval_msq_host(soa.pin_memory(), out, P)
+    assert torch.equal(out, dev.cpu())
+    idx = np.unique(np.concatenate([np.arange(0, 50), np.arange((1 << 18) - 50, (1 << 18) + 50),
+                                    np.arange(2 * (1 << 18) - 50, 2 * (1 << 18) + 50), np.arange(P - 50, P)]))
+    ref = oracle.msq(1, n, mom[idx].numpy())
+    assert np.max(np.abs(out.numpy()[idx] / ref - 1)) <= TOL
+    out2 = torch.full((P,), float("nan"), dtype=torch.float64)
+    proc.eval_msq_host(soa.contiguous(), out2, P)
+    assert torch.equal(out2, out)
+
+
 def test_two_streams_two_handles(qed):
     n = 2
     mom = synthetic.rambo_cm(n, 20000, seed=9000)
