@@ -244,10 +244,58 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
 // phi of one sigma stays in registers across the tau loop; loops are rolled so that ptxas
 // cannot hoist every leaf load of the subset (which spills).
 // hh: packed (2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1)) of this lane and subset (gen tables)
-template <class T, int AS>
+// SB > 1: SB sigma rows of phi stay in registers across the tau loop (1/SB of the ubar reloads)
+template <class T, int AS, int SB>
+__device__ __forceinline__ void join_set_sb(const double* __restrict__ base, int h0, int h1, int o0, int o1,
+                                            double (&acc)[AS][8]) {
+  static_assert(T::NSIG % SB == 0, "sigma blocking must divide NSIG");
+#pragma unroll 1
+  for (int sg = 0; sg < T::NSIG; sg += SB) {
+    c2 p0[SB][4], p1[SB][4];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const double* prow = base + T::PHI + (sg + b) * 4 * T::NHI * 2;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        p0[b][c] = ld2(prow + c * T::NHI * 2 + h0);
+        p1[b][c] = ld2(prow + c * T::NHI * 2 + h1);
+      }
+    }
+#pragma unroll 1
+    for (int tu = 0; tu < T::NTAU; ++tu) {
+      const double* urow = base + T::UBL + tu * 4 * T::NHO * 2;
+      c2 u0[4], u1[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        u0[c] = ld2(urow + c * T::NHO * 2 + o0);
+        u1[c] = ld2(urow + c * T::NHO * 2 + o1);
+      }
+#pragma unroll
+      for (int b = 0; b < SB; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double* A = acc[(c + b * (AS > 2 ? 2 : 1)) % AS];
+          A[0] = fma(u0[c].r, p0[b][c].r, fma(-u0[c].i, p0[b][c].i, A[0]));
+          A[1] = fma(u0[c].r, p0[b][c].i, fma(u0[c].i, p0[b][c].r, A[1]));
+          A[2] = fma(u0[c].r, p1[b][c].r, fma(-u0[c].i, p1[b][c].i, A[2]));
+          A[3] = fma(u0[c].r, p1[b][c].i, fma(u0[c].i, p1[b][c].r, A[3]));
+          A[4] = fma(u1[c].r, p0[b][c].r, fma(-u1[c].i, p0[b][c].i, A[4]));
+          A[5] = fma(u1[c].r, p0[b][c].i, fma(u1[c].i, p0[b][c].r, A[5]));
+          A[6] = fma(u1[c].r, p1[b][c].r, fma(-u1[c].i, p1[b][c].i, A[6]));
+          A[7] = fma(u1[c].r, p1[b][c].i, fma(u1[c].i, p1[b][c].r, A[7]));
+        }
+    }
+  }
+}
+
+template <class T, int AS, int SB = 1>
 __device__ __forceinline__ void join_set(const double* __restrict__ base, unsigned hh, double (&acc)[AS][8], int lb = 0) {
   const int h0 = hh & 255, h1 = (hh >> 8) & 255, o0 = (hh >> 16) & 255, o1 = hh >> 24;
   base += lb * T::LEAFB;   // leaf buffer of the lb-th subset of a batch (T::SETB subsets per stage)
+  if constexpr (SB > 1) {
+    join_set_sb<T, AS, SB>(base, h0, h1, o0, o1, acc);
+    return;
+  }
 #pragma unroll 1
   for (int sg = 0; sg < T::NSIG; ++sg) {
     c2 p0[4], p1[4];
@@ -319,7 +367,7 @@ __device__ __forceinline__ void join_set_hs(const double* __restrict__ base, uin
 
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
-template <class T, int AS = 2>
+template <class T, int AS = 2, int SB = 1>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
@@ -368,7 +416,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     group_sync<T>(pb);
 #pragma unroll
     for (int lb = 0; lb < T::SETB; ++lb)   // padding subsets of a ragged last batch: leaves only, no join
-      if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS>(base, T::hiho(s0 + lb, g), acc, lb);
+      if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS, SB>(base, T::hiho(s0 + lb, g), acc, lb);
     group_sync<T>(pb);
   }
 #pragma unroll
@@ -440,7 +488,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
     }
     group_sync<T>(pb);
     double amp[2 * T::NAMP];
-    eval_point<T, V::AS>(base, g, pb, a, amp);
+    eval_point<T, V::AS, V::SB>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
       if (valid && holds_amps<T>(g)) {

@@ -41,13 +41,23 @@ def choose_launch(plan: Plan) -> tuple[int, int]:
 
 def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     """Launch variants compiled into the library, selected at run time with QED_VARIANT:
-    (warps per block, min resident blocks, accumulator split AS, L2 prefetch).  Variant 0 is
+    (warps per block, min resident blocks, accumulator split AS, L2 prefetch, sigma block SB).  Variant 0 is
     the default (chosen from measurements)."""
     wpb, mb = choose_launch(plan)
     mb4 = max(1, min(mb, 65536 // (152 * wpb * 32)))
     if plan.N >= 5:   # r01 sweep: 4 partial accumulators win for n >= 4
-        return [(wpb, mb4, 4, 1), (wpb, mb, 2, 1), (wpb, mb, 2, 0)]
-    return [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
+        vs = [(wpb, mb4, 4, 1), (wpb, mb, 2, 1), (wpb, mb, 2, 0)]
+    else:
+        vs = [(wpb, mb, 2, 1), (wpb, mb4, 4, 1), (wpb, mb, 2, 0)]
+    vs = [v + (1,) for v in vs]
+    if plan.n_sigma % 2 == 0:   # sigma blocked in the join (SB phi rows held across the tau loop)
+        mb6 = max(1, min(mb, 65536 // (184 * wpb * 32)))
+        sb = [(wpb, mb6, 4, 1, 2), (wpb, mb4, 2, 1, 2)]
+        if plan.n_sigma % 3 == 0:
+            sb.append((wpb, max(1, min(mb, 65536 // (216 * wpb * 32))), 4, 1, 3))
+        # r22 sweep: SB = 2 wins at n = 4 (+6 %) and n = 5 (+5 %), loses at n = 3
+        vs = sb + vs if plan.N >= 5 else vs + sb
+    return vs
 
 
 def _tasks(name, tasks):
@@ -158,8 +168,8 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     bodies = "\n".join(emit_plan_namespace(p, ns) for p, ns in zip(plans, nss))
     variant_structs = "".join(
-        f"namespace {nss[pi]} {{ struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }}; }}\n"
-        for i, (pi, w, m, a, p) in enumerate(vs))
+        f"namespace {nss[pi]} {{ struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}, SB = {sb}; }}; }}\n"
+        for i, (pi, w, m, a, p, sb) in enumerate(vs))
     kernel_cases = "\n".join(
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, false>;"

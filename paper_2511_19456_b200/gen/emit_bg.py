@@ -92,7 +92,7 @@ def emit_bg_source(plan: BGPlan) -> str:
     hst = hs_table(plan) if plan.hs == 2 else [0, 0]
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}" for k, v in plan.flops.items())
     lay = ", ".join(f"{k} = {L[k]}" for k in ("MOM", "RED", "EPS", "MASK", "U", "UB", "PHI", "UBL"))
-    variant_structs = "".join(f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}; }};\n"
+    variant_structs = "".join(f"struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}, SB = 1; }};\n"
                               for i, (w, m, a, p) in enumerate(vs))
     kcases = "\n".join(
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{i}, true>\n"
