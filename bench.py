@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=2)
+    ap.add_argument("--n", "--photons", dest="n", type=int, default=2,
+                    help="outgoing photons (--photons under torchrun, whose parser claims --n)")
     ap.add_argument("--points", type=int, default=1 << 22, help="points per GPU")
     ap.add_argument("--sqrt-s", type=float, default=5.0)
     ap.add_argument("--seed", type=int, default=2)
@@ -97,6 +98,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- distributed plumbing
+DIST_BACKEND = os.environ.get("QED_BENCH_DIST_BACKEND", "nccl")   # "gloo": multi-rank plumbing test on one GPU
 def dist_setup(gpus: int):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -104,11 +106,18 @@ def dist_setup(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "gloo":
+            # plumbing check on a box with fewer GPUs than ranks (tests only: ranks share devices,
+            # so the timings are not scaling numbers)
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
-    return world, rank, local
+    # device of this rank (== local_rank except in the gloo plumbing test, where ranks share devices)
+    return world, rank, (torch.cuda.current_device() if torch.cuda.is_available() else local)
 
 
 def barrier(world):
@@ -122,7 +131,7 @@ def max_over_ranks(world, x: float) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if DIST_BACKEND == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
