@@ -47,8 +47,9 @@ def _compile(src: str, force: bool) -> str:
     log = os.path.join(LIB_DIR, "ptxas_" + os.path.basename(src).replace(".cu", ".log"))
     cmd = [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", obj + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    with open(log, "w") as f:   # (compile-time lines dropped: the tracked logs change only with the code)
+        text = r.stdout + r.stderr
+        f.write(" ".join(cmd) + "\n" + "".join(ln for ln in text.splitlines(True) if "Compile time" not in ln))
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
     os.replace(obj + ".tmp", obj)
