@@ -14,9 +14,11 @@ import synthetic  # noqa: E402
 from paper_2511_19456_b200 import mc, qed  # noqa: E402
 
 torch.cuda.set_device(0)
-cases = [("cdag", n, 37) for n in (1, 2, 3, 4, 5)] + [("bg", n, 19) for n in (1, 2, 3, 4, 5, 6, 7)]
+cases = [("cdag", n, 37) for n in (1, 2, 3, 4, 5)] + [("bg", n, 19) for n in (1, 2, 3, 4, 5, 6, 7)] + [("bg", 8, 2)]
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
-    cases = [("cdag", 2, 37), ("cdag", 3, 21), ("cdag", 5, 3), ("bg", 5, 3), ("bg", 7, 2)]
+    # racecheck: shared-memory staging of every kernel shape (two-half joins at bg n = 6, 8)
+    cases = [("cdag", 2, 37), ("cdag", 3, 21), ("cdag", 4, 5), ("cdag", 5, 3), ("bg", 5, 3), ("bg", 6, 3),
+             ("bg", 7, 2), ("bg", 8, 1)]
 for algo, n, npts in cases:
     mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=5 + n)
     soa = synthetic.to_soa(mom).cuda()
@@ -28,6 +30,9 @@ for algo, n, npts in cases:
     if n <= 5:
         part = torch.zeros(3 * mc.n_chunks(mc.CHUNK + npts), dtype=torch.float64, device="cuda")
         proc.mc_sum(part, 5.0, 0.25, 3, mc.CHUNK - 5, npts)
+    if n <= 2:   # host entry point (pinned staging, two streams)
+        hout = torch.empty(npts, dtype=torch.float64).pin_memory()
+        proc.eval_msq_host(soa.cpu().pin_memory(), hout, npts)
     torch.cuda.synchronize()
     assert torch.isfinite(out).all(), (algo, n)
     print(algo, n, "ok", flush=True)
