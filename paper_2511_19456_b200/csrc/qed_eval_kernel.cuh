@@ -382,13 +382,16 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
 #pragma unroll 1
     for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
+      uint2 ww[T::SETB / 2];   // join offsets: loaded before the leaf stage so their latency overlaps it
+#pragma unroll
+      for (int lb = 0; lb < T::SETB; lb += 2) ww[lb / 2] = T::hs_offsets(s0 + lb + q, gh);
       T::run_set(base, g, pb, s0);
       group_sync<T>(pb);
 #pragma unroll
       for (int lb = 0; lb < T::SETB; lb += 2) {
         const int si = s0 + lb + q;
         if (T::NSETS_REAL % T::SETB == 0 || si < T::NSETS_REAL) {
-          const uint2 w = T::hs_offsets(si, gh);
+          const uint2 w = ww[lb / 2];
           if ((T::set_mask(si) >> (T::N - 1)) & 1) join_set_hs<T, true>(base, w, acc, lb + q);
           else join_set_hs<T, false>(base, w, acc, lb + q);
         }
@@ -412,11 +415,14 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
 #pragma unroll 1
   for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
+    unsigned hh[T::SETB];   // join offsets: loaded before the leaf stage so their latency overlaps it
+#pragma unroll
+    for (int lb = 0; lb < T::SETB; ++lb) hh[lb] = T::hiho(s0 + lb, g);
     T::run_set(base, g, pb, s0);      // leaves of subsets s0 .. s0 + SETB - 1
     group_sync<T>(pb);
 #pragma unroll
     for (int lb = 0; lb < T::SETB; ++lb)   // padding subsets of a ragged last batch: leaves only, no join
-      if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS, SB>(base, T::hiho(s0 + lb, g), acc, lb);
+      if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS, SB>(base, hh[lb], acc, lb);
     group_sync<T>(pb);
   }
 #pragma unroll
