@@ -192,6 +192,27 @@ __device__ __forceinline__ void run_tasks(double* base, int g, const ushort4* __
     if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
 }
 
+// run_tasks split in two (T::SD / load_set / run_set_d): descriptors of one task list into registers ...
+template <class T, int COUNT, int OFF>
+__device__ __forceinline__ void load_tasks(ushort4 (&d)[(COUNT + T::G - 1) / T::G], int g, const ushort4* __restrict__ tbl) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k) {
+    const int t = gl + k * T::G;
+    d[k] = (t < COUNT) ? tbl[t] : make_ushort4(0, 0, 0, 0);
+  }
+}
+// ... and the tasks themselves
+template <class T, int COUNT, class F, int OFF>
+__device__ __forceinline__ void exec_tasks(double* base, int g, const ushort4 (&d)[(COUNT + T::G - 1) / T::G], F f) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k)
+    if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
+}
+
 template <class T>
 __device__ __forceinline__ void group_sync(int pb) {
   if constexpr (T::G <= 32) {
@@ -367,7 +388,17 @@ __device__ __forceinline__ void join_set_hs(const double* __restrict__ base, uin
 
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
-template <class T, int AS = 2, int SB = 1>
+// launch-variant field DP (descriptor prefetch, CDAG plans only); variants without it read 0
+template <class V, class = void>
+struct dp_of {
+  static constexpr int value = 0;
+};
+template <class V>
+struct dp_of<V, decltype(void(V::DP))> {
+  static constexpr int value = V::DP;
+};
+
+template <class T, int AS = 2, int SB = 1, int DP = 0>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
@@ -413,6 +444,21 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
   for (int q = 0; q < AS; ++q)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
+  if constexpr (DP) {
+    // leaf-stage descriptors one subset ahead: subset s0 + 1's are loaded before subset s0's joins
+    static_assert(T::SETB == 1, "descriptor prefetch: one subset per leaf stage");
+    typename T::SD sd;
+    T::load_set(sd, g, 0);
+#pragma unroll 1
+    for (int s0 = 0; s0 < T::NSETS; ++s0) {
+      const unsigned hh = T::hiho(s0, g);
+      T::run_set_d(base, g, pb, sd);
+      group_sync<T>(pb);
+      if (s0 + 1 < T::NSETS) T::load_set(sd, g, s0 + 1);
+      join_set<T, AS, SB>(base, hh, acc, 0);
+      group_sync<T>(pb);
+    }
+  } else {
 #pragma unroll 1
   for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
     unsigned hh[T::SETB];   // join offsets: loaded before the leaf stage so their latency overlaps it
@@ -424,6 +470,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     for (int lb = 0; lb < T::SETB; ++lb)   // padding subsets of a ragged last batch: leaves only, no join
       if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS, SB>(base, hh[lb], acc, lb);
     group_sync<T>(pb);
+  }
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -482,19 +529,43 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
   double* base = smem + pb * T::STRIDE;
   const long long n = a.n_points;
   const long long stride_pts = (long long)gridDim.x * PB;
+  // PF == 2: the next point's momenta are loaded into registers (MR per lane) while this point is evaluated
+  constexpr int MR = (4 * (T::N + 2) + G - 1) / G;
+  double mnext[MR];
+  if (V::PF == 2) {
+    const long long pt = (long long)blockIdx.x * PB + pb;
+    const long long ptc = pt < n ? pt : n - 1;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int t = g + k * G;
+      mnext[k] = t < 4 * (T::N + 2) ? __ldg(a.mom + (long long)t * n + ptc) : 0.0;
+    }
+  }
 #pragma unroll 1
   for (long long p0 = (long long)blockIdx.x * PB; p0 < n; p0 += stride_pts) {
     const long long pt = p0 + pb;
     const bool valid = pt < n;
     const long long ptc = valid ? pt : n - 1;
     // stage 0: momenta, SoA layout mom[(4 j + mu) n + i]; L2 prefetch of the next batch
-    for (int t = g; t < 4 * (T::N + 2); t += G) {
-      base[T::MOM + t] = __ldg(a.mom + (long long)t * n + ptc);
-      if (V::PF && pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
+    if (V::PF == 2) {
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (g + k * G < 4 * (T::N + 2)) base[T::MOM + g + k * G] = mnext[k];
+      const long long nx = pt + stride_pts < n ? pt + stride_pts : n - 1;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int t = g + k * G;
+        if (t < 4 * (T::N + 2)) mnext[k] = __ldg(a.mom + (long long)t * n + nx);
+      }
+    } else {
+      for (int t = g; t < 4 * (T::N + 2); t += G) {
+        base[T::MOM + t] = __ldg(a.mom + (long long)t * n + ptc);
+        if (V::PF && pt + stride_pts < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mom + (long long)t * n + pt + stride_pts));
+      }
     }
     group_sync<T>(pb);
     double amp[2 * T::NAMP];
-    eval_point<T, V::AS, V::SB>(base, g, pb, a, amp);
+    eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
       if (valid && holds_amps<T>(g)) {

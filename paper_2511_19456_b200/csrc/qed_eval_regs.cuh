@@ -70,6 +70,13 @@ __device__ __forceinline__ void mask_store(const double* p, const double (&q)[N]
   reinterpret_cast<double2*>(out)[2] = make_double2(Q3 * inv, 0.0);
 }
 
+// propagator constants of S(Q) for the one-photon subset {i}: Q = p + sg k_i  -> out[5] in registers
+__device__ __forceinline__ void mask_regs(const double* p, const double* k, double sg, double (&out)[5]) {
+  const double Q0 = fma(sg, k[0], p[0]), Q1 = fma(sg, k[1], p[1]), Q2 = fma(sg, k[2], p[2]), Q3 = fma(sg, k[3], p[3]);
+  const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;
+  const double inv = 1.0 / D;
+  out[0] = (Q0 + 1.0) * inv; out[1] = (1.0 - Q0) * inv; out[2] = Q1 * inv; out[3] = Q2 * inv; out[4] = Q3 * inv;
+}
 
 // Shared-memory spinor load that the compiler may not hoist, merge or cache in registers:
 // the phi leaves are re-read per out-side block so that only one phi spinor is live at a time.
@@ -151,6 +158,16 @@ __device__ __forceinline__ void cdot8_acc(const spinor& l0, const spinor& l1, co
   }
 }
 
+// T::PASSES (bodies that hand their amplitudes over pass by pass); 1 when absent
+template <class T, class = void>
+struct passes_of {
+  static constexpr int value = 1;
+};
+template <class T>
+struct passes_of<T, decltype(void(T::PASSES))> {
+  static constexpr int value = T::PASSES;
+};
+
 template <class T, class V, bool PER_CONFIG>
 __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(QedEvalArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -198,36 +215,45 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
         asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
       }
     }
-    double acc[2 * NACC];
+    // amplitudes of NACC configurations -> per-configuration |M|^2 stores, or this thread's part of the sum
+    double sum = 0.0;
+    auto fin = [&](const double (&acc)[2 * NACC], int sub_) {
+      if (PER_CONFIG) {
+        if (valid) {
 #pragma unroll
-    for (int i = 0; i < 2 * NACC; ++i) acc[i] = 0.0;
-    T::body(msrc, mstride, mpt, sub, sl, a, acc);
-    if (PER_CONFIG) {
-      if (valid) {
+          for (int idx = 0; idx < NACC; ++idx) {
+            const unsigned h = T::config_of(idx, sub_);
+            if (h == 0xffffffffu) continue;   // duplicate holder of this amplitude (split bodies)
+            unsigned hx = 0;
 #pragma unroll
-        for (int idx = 0; idx < NACC; ++idx) {
-          const unsigned h = T::config_of(idx, sub);
-          if (h == 0xffffffffu) continue;   // duplicate holder of this amplitude (split bodies)
-          unsigned hx = 0;
-#pragma unroll
-          for (int b = 0; b < N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
-          a.out[pt * (1LL << (N + 2)) + hx] = a.coupling * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+            for (int b = 0; b < N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
+            a.out[pt * (1LL << (N + 2)) + hx] = a.coupling * fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
+          }
         }
-      }
-    } else {
-      double sum = 0.0;
-      if (a.fixed_mask == 0) {
+      } else if (a.fixed_mask == 0) {
+        double part = 0.0;
 #pragma unroll
-        for (int idx = 0; idx < NACC; ++idx) sum = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], sum));
-        if (T::config_of(0, sub) == 0xffffffffu) sum = 0.0;
+        for (int idx = 0; idx < NACC; ++idx) part = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], part));
+        if (T::config_of(0, sub_) != 0xffffffffu) sum += part;
       } else {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {
-          const unsigned h = T::config_of(idx, sub);
+          const unsigned h = T::config_of(idx, sub_);
           const double t = fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
           sum += ((h & a.fixed_mask) == a.fixed_val) ? t : 0.0;
         }
       }
+    };
+    if constexpr (passes_of<T>::value > 1) {
+      T::body_passes(msrc, mstride, mpt, sl, a, fin);   // calls fin once per pass
+    } else {
+      double acc[2 * NACC];
+#pragma unroll
+      for (int i = 0; i < 2 * NACC; ++i) acc[i] = 0.0;
+      T::body(msrc, mstride, mpt, sub, sl, a, acc);
+      fin(acc, sub);
+    }
+    if (!PER_CONFIG) {
 #pragma unroll
       for (int o = 1; o < TPP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       if (valid && sub == 0) a.out[pt] = a.norm * sum;

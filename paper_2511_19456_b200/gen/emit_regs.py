@@ -155,6 +155,147 @@ def emit_regs_body(N: int) -> str:
     return "\n".join(L) + "\n"
 
 
+def emit_regs_body1(N: int) -> str:
+    """N = 2 body with ONE thread per point: the thread holds all 16 amplitudes and the four phi leaves
+    of the current in-side photon in registers, so no shared-memory exchange and no warp fences.
+    Same DAG, same flops as emit_regs_body(2) (nothing is recomputed)."""
+    assert N == 2
+    L = []
+    w = L.append
+    w("// ---- generated straight-line body, N = 2 (thread = point), j = 1, everything in registers")
+    w("template <class ARGS>")
+    w("__device__ __forceinline__ void regs_body1_N2(const double* __restrict__ mom, long long n, long long pt, int,")
+    w("                                               double* __restrict__, const ARGS& a, double (&acc)[32]) {")
+    w("  const int e_out = a.e_out_particle;")
+    w("  double pe[4], pp[4], q[2][4];")
+    w("  for (int mu = 0; mu < 4; ++mu) {")
+    w("    pe[mu] = qed::ld_mom(mom + (long long)mu * n + pt);")
+    w("    pp[mu] = qed::ld_mom(mom + (long long)(4 * e_out + mu) * n + pt);")
+    w("  }")
+    w("  for (int i = 0; i < 2; ++i) {")
+    w("    const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("    for (int mu = 0; mu < 4; ++mu) q[i][mu] = qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w("  }")
+    w("  // U: eps(k_i, lam) (lam = 1 transverse, eps^3 = 0), propagator constants of S(Q_{i}), u, ubar")
+    w("  double e[2][2][3], m[2][5];")
+    w("  for (int i = 0; i < 2; ++i) {")
+    w("    double ct, st, cf, sf;")
+    w("    qed::eps_consts(q[i], ct, st, cf, sf);")
+    w("    e[i][0][0] = ct * cf; e[i][0][1] = ct * sf; e[i][0][2] = -st;")
+    w("    e[i][1][0] = -sf; e[i][1][1] = cf; e[i][1][2] = 0.0;")
+    w("  }")
+    w("  for (int i = 0; i < 2; ++i) {")
+    w("    const double sg = i < a.n_in_ph ? 1.0 : -1.0;")
+    w("    qed::mask_regs(pe, q[i], sg, m[i]);")
+    w("  }")
+    w("  const qed::spinor u0 = qed::u_spinor(pe, 0), u1 = qed::u_spinor(pe, 1);")
+    w("  const qed::spinor ub0 = qed::ubar_spinor(pp, 0), ub1 = qed::ubar_spinor(pp, 1);")
+    for a_ in range(2):
+        b = 1 - a_
+        w(f"  {{  // in-side photon {a_}: phi[s][lam_{a_}] = S(Q_{a_}) epsslash u(p, s); out-side leaves ubar(s') epsslash_{b}")
+        w("    qed::spinor ph[2][2];")
+        for s, us in ((0, "u0"), (1, "u1")):
+            w(f"    ph[{s}][0] = qed::prop_col(m[{a_}], qed::eslash_col(e[{a_}][0], {us}));")
+            w(f"    ph[{s}][1] = qed::prop_col(m[{a_}], qed::eslash_col_t(e[{a_}][1], {us}));")
+        for lb in range(2):
+            for sp, ubs in ((0, "ub0"), (1, "ub1")):
+                w(f"    {{ const qed::spinor leaf = qed::eslash_row{T_[lb]}(e[{b}][{lb}], {ubs});")
+                for s in range(2):
+                    for la in range(2):
+                        idx = s | (la << (1 + a_)) | (lb << (1 + b)) | (sp << 3)
+                        w(f"      qed::cdot_acc(leaf, ph[{s}][{la}], acc[{2 * idx}], acc[{2 * idx + 1}]);")
+                w("    }")
+        w("  }")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
+def emit_regs_body1p(N: int, fence: bool = True) -> str:
+    """N = 3 body with ONE thread per point, in two passes over the outgoing-electron spin s'.
+    The thread's 12 phi leaves go to a private shared-memory slot (no exchange, no sharing); each pass
+    walks the out-side trie of u-bar(p', s') depth first with the 32 amplitudes of that s' in registers
+    and hands them to `fin` (|amp|^2 or per-configuration store) before the next pass reuses them.
+    Same DAG, same flops as emit_regs_body(3) (nothing is recomputed)."""
+    assert N == 3
+    L = []
+    w = L.append
+    fn = "regs_body1p_N3" if fence else "regs_body1q_N3"
+    w(f"// ---- generated straight-line body, N = 3 (thread = point, two passes over s'), j = 1")
+    w("template <class ARGS, class FIN>")
+    w(f"__device__ __forceinline__ void {fn}(const double* __restrict__ mom, long long n, long long pt,")
+    w("                                               double* __restrict__ sl, const ARGS& a, FIN&& fin) {")
+    w("  const int e_out = a.e_out_particle;")
+    w("  double pe[4], pp[4], q[3][4], sg[3];")
+    w("  for (int mu = 0; mu < 4; ++mu) {")
+    w("    pe[mu] = qed::ld_mom(mom + (long long)mu * n + pt);")
+    w("    pp[mu] = qed::ld_mom(mom + (long long)(4 * e_out + mu) * n + pt);")
+    w("  }")
+    w("  for (int i = 0; i < 3; ++i) {")
+    w("    const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("    sg[i] = i < a.n_in_ph ? 1.0 : -1.0;")
+    w("    for (int mu = 0; mu < 4; ++mu) q[i][mu] = qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w("  }")
+    w("  double e[3][2][3];")
+    w("  for (int i = 0; i < 3; ++i) {")
+    w("    double ct, st, cf, sf;")
+    w("    qed::eps_consts(q[i], ct, st, cf, sf);")
+    w("    e[i][0][0] = ct * cf; e[i][0][1] = ct * sf; e[i][0][2] = -st;")
+    w("    e[i][1][0] = -sf; e[i][1][1] = cf; e[i][1][2] = 0.0;")
+    w("  }")
+    w("  // in-side leaves phi_a[s][lam] = S(Q_{a}) epsslash_a(lam) u(p, s) -> private slot, spinor a * 4 + s * 2 + lam")
+    w("  {")
+    w("    const qed::spinor u0 = qed::u_spinor(pe, 0), u1 = qed::u_spinor(pe, 1);")
+    for a_ in range(3):
+        w(f"    {{ double m[5]; qed::mask_regs(pe, q[{a_}], sg[{a_}], m);")
+        for s_, us in ((0, "u0"), (1, "u1")):
+            for lam in range(2):
+                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::prop_col(m, qed::eslash_col{T_[lam]}(e[{a_}][{lam}], {us})));")
+        w("    }")
+    w("  }")
+    w("  // propagator constants of S(Q_{all \\ b}): Q = p + sum_{i != b} sg_i k_i")
+    w("  double mc[3][5];")
+    w("  for (int b = 0; b < 3; ++b) {")
+    w("    double Q0 = pe[0], Q1 = pe[1], Q2 = pe[2], Q3 = pe[3];")
+    w("    for (int i = 0; i < 3; ++i)")
+    w("      if (i != b) { Q0 = fma(sg[i], q[i][0], Q0); Q1 = fma(sg[i], q[i][1], Q1); Q2 = fma(sg[i], q[i][2], Q2); Q3 = fma(sg[i], q[i][3], Q3); }")
+    w("    const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;")
+    w("    const double inv = 1.0 / D;")
+    w("    mc[b][0] = (Q0 + 1.0) * inv; mc[b][1] = (1.0 - Q0) * inv; mc[b][2] = Q1 * inv; mc[b][3] = Q2 * inv; mc[b][4] = Q3 * inv;")
+    w("  }")
+    w("  #pragma unroll 1")
+    w("  for (int sp = 0; sp < 2; ++sp) {")
+    w("    double acc[32];")
+    w("    #pragma unroll")
+    w("    for (int i = 0; i < 32; ++i) acc[i] = 0.0;")
+    w("    const qed::spinor ub = qed::ubar_spinor(pp, sp);")
+    for b in range(3):
+        for lb in range(2):
+            w(f"    {{  // tau_1 = photon {b}, lam_{b} = {lb}")
+            w(f"      const qed::spinor I = qed::prop_row(mc[{b}], qed::eslash_row{T_[lb]}(e[{b}][{lb}], ub));")
+            for c in range(3):
+                if c == b:
+                    continue
+                a_ = 3 - b - c
+                w(f"      {{  // tau_2 = photon {c}, remaining photon {a_}")
+                if fence:
+                    w("        __syncwarp();  // scheduling fence: keeps ptxas from hoisting every phi load")
+                w(f"        const qed::spinor l0 = qed::eslash_row(e[{c}][0], I);")
+                w(f"        const qed::spinor l1 = qed::eslash_row_t(e[{c}][1], I);")
+                w("        #pragma unroll")
+                w("        for (int k = 0; k < 4; ++k) {")
+                w(f"          const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
+                w(f"          const int i0 = (k >> 1) | ((k & 1) << {1 + a_}) | ({lb} << {1 + b});")
+                w("          qed::cdot_acc(l0, ph, acc[2 * i0], acc[2 * i0 + 1]);")
+                w(f"          qed::cdot_acc(l1, ph, acc[2 * (i0 | {1 << (1 + c)})], acc[2 * (i0 | {1 << (1 + c)}) + 1]);")
+                w("        }")
+                w("      }")
+            w("    }")
+    w("    fin(acc, sp);")
+    w("  }")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
 def emit_regs_body4(N: int) -> str:
     """N = 3 body with four threads per point: thread = (point, s', lam_0).  Photon 0's polarisation
     is fixed per thread, so out-side nodes that do not involve photon 0 are computed by both lam_0
@@ -297,8 +438,8 @@ def emit_regs_source(N: int) -> str:
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, false>;"
         for i, (d, w, m, p) in enumerate(vs))
-    tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "2" for d, *_ in vs) + "}"
-    body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) if N == 3 else ""
+    tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "1" if d.startswith("T1") else "2" for d, *_ in vs) + "}"
+    body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) + "\n" + emit_regs_body1p(N) if N == 3 else ""
     t4 = f"""
 // four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
 struct T4 {{
@@ -319,7 +460,30 @@ struct TI : T {{
                                               const ARGS2& a, double (&acc)[{2 << (N + 1)}]) {{
     regs_bodyi_N{N}(mom, n, pt, sub, sl, a, acc);
   }}
+}};
+// one thread per point, two passes over s' (32 amplitudes live per pass), phi in a private slot
+struct T1P {{
+  static constexpr int N = {N}, TPP = 1, NACC = {1 << (N + 1)}, STRIDE = 98, PASSES = 2;
+  template <class ARGS2, class FIN>
+  static __device__ __forceinline__ void body_passes(const double* mom, long long n, long long pt, double* sl,
+                                                     const ARGS2& a, FIN&& fin) {{
+    regs_body1p_N{N}(mom, n, pt, sl, a, fin);
+  }}
+  static __device__ __forceinline__ unsigned config_of(int idx, int sub) {{ return idx | ((unsigned)sub << (N + 1)); }}
 }};""" if N == 3 else ""
+    if N == 2:
+        body4 = emit_regs_body1(N)
+        t4 = f"""
+// one thread per point: all 16 amplitudes and the phi leaves in registers, no shared-memory slot
+struct T1 {{
+  static constexpr int N = {N}, TPP = 1, NACC = {1 << (N + 2)}, STRIDE = 0;
+  template <class ARGS2>
+  static __device__ __forceinline__ void body(const double* mom, long long n, long long pt, int sub, double* sl,
+                                              const ARGS2& a, double (&acc)[{2 << (N + 2)}]) {{
+    regs_body1_N{N}(mom, n, pt, sub, sl, a, acc);
+  }}
+  static __device__ __forceinline__ unsigned config_of(int idx, int) {{ return idx; }}
+}};"""
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_regs.py -- do not edit.
 // Register-resident kernel for N = {N} photons (n = {N - 1}); thread = (point, s') [T] or (point, s', lam_0) [T4].
 // Algorithmic FP64 flops per point:
@@ -357,7 +521,8 @@ void qedregs_config_N{N}(int variant, int* warps_per_block, int* points_per_warp
   *warps_per_block = wpb[variant];
   *points_per_warp = 32 / tpp[variant];
   static const int pf[{len(vs)}] = {{{", ".join(str(v[3]) for v in vs)}}};
-  *smem_per_block = (long long)wpb[variant] * (32 / tpp[variant]) * {ns}::T::STRIDE * 8 +
+  static const int stride[{len(vs)}] = {{{", ".join(f"{ns}::{v[0]}::STRIDE" if v[0].startswith("T1") else f"{ns}::T::STRIDE" for v in vs)}}};
+  *smem_per_block = (long long)wpb[variant] * (32 / tpp[variant]) * stride[variant] * 8 +
                     (pf[variant] == 2 ? (long long)wpb[variant] * 2 * {4 * (N + 2)} * (32 / tpp[variant]) * 8 : 0);
   *flops_per_point = {ns}::T::FLOPS_PER_POINT;
 }}
@@ -370,9 +535,12 @@ def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
     Variant 0 = best of the latest sweep (profiles/sweep_*.jsonl)."""
     if N == 3:
         # r20 sweep: the interleaved join body TI >= T at n = 2 once the transverse vertices shortened T
-        return [("TI", 4, 1, 2), ("T", 4, 1, 2), ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1),
-                ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
-    return [("T", 2, 6, 2), ("T", 4, 1, 0), ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
+        # r28 sweep: one thread per point in two s' passes (T1P) 2.31e9 pts/s (62.5 %) vs 2.01e9 for TI
+        return [("T1P", 8, 1, 1), ("T1P", 8, 1, 0), ("T1P", 4, 2, 1), ("TI", 4, 1, 2), ("T", 4, 1, 2), ("T", 4, 1, 1),
+                ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
+    # t1 sweep: one thread per point (T1) 1.19e10 pts/s (68 % of FP64 peak) vs 8.18e9 for T
+    return [("T1", 8, 1, 2), ("T1", 4, 2, 2), ("T1", 2, 4, 2), ("T1", 4, 2, 1), ("T", 2, 6, 2), ("T", 4, 1, 0),
+            ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
 
 
 def generate_regs(out_dir: str, Ns=(2, 3)) -> list[str]:
