@@ -398,24 +398,12 @@ struct dp_of<V, decltype(void(V::DP))> {
   static constexpr int value = V::DP;
 };
 
-struct NoID {};
-template <class T, bool HAS>
-struct id_of {
-  using type = NoID;
-};
-template <class T>
-struct id_of<T, true> {
-  using type = typename T::ID;
-};
-
-// DP bit 0: leaf-stage descriptors one subset ahead; bit 1: interior descriptors from `id` (registers)
-template <class T, int AS = 2, int SB = 1, int DP = 0, class IDT = NoID>
-__device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP],
-                                           const IDT& id = IDT{}) {
+// DP: leaf-stage descriptors loaded one subset ahead (T::SD / load_set / run_set_d)
+template <class T, int AS = 2, int SB = 1, int DP = 0>
+__device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
-  if constexpr (DP & 2) T::run_interiors_d(base, g, pb, id);
-  else T::run_interiors(base, g, pb);
+  T::run_interiors(base, g, pb);
   if constexpr (T::HS == 2) {
     // half q joins subsets s0 + q, s0 + q + 2, ... of every batch; the halves' partial amplitudes are
     // summed into half 0 at the end through shared memory (the dead U.. region of the point's slot)
@@ -457,7 +445,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
   for (int q = 0; q < AS; ++q)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
-  if constexpr (DP & 1) {
+  if constexpr (DP) {
     // leaf-stage descriptors one subset ahead: subset s0 + 1's are loaded before subset s0's joins
     static_assert(T::SETB == 1, "descriptor prefetch: one subset per leaf stage");
     typename T::SD sd;
@@ -542,9 +530,6 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
   double* base = smem + pb * T::STRIDE;
   const long long n = a.n_points;
   const long long stride_pts = (long long)gridDim.x * PB;
-  using IDT = typename id_of<T, (dp_of<V>::value & 2) != 0>::type;
-  IDT id;
-  if constexpr (dp_of<V>::value & 2) T::load_interiors(id, g);
   // PF == 2: the next point's momenta are loaded into registers (MR per lane) while this point is evaluated
   constexpr int MR = (4 * (T::N + 2) + G - 1) / G;
   double mnext[MR];
@@ -581,8 +566,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
     }
     group_sync<T>(pb);
     double amp[2 * T::NAMP];
-    if constexpr (dp_of<V>::value & 2) eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp, id);
-    else eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
+    eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
     if (PER_CONFIG) {
       if (valid && holds_amps<T>(g)) {

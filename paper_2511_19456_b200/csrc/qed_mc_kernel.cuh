@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
       }
       group_sync<T>(pb);
       double amp[2 * T::NAMP];
-      eval_point<T, V::AS, V::SB, dp_of<V>::value & 1>(base, g, pb, a, amp);
+      eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
       const double msq = group_msq<T>(amp, g, pb, base, a);
       if (g == 0) {
         const double v = (valid && pass) ? w * msq : 0.0;

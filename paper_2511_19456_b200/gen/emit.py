@@ -60,10 +60,10 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     # DP = 1: leaf-stage descriptors one subset ahead; PF = 2: next point's momenta prefetched into registers
     vs = [v + (0,) for v in vs]
     vs += [vs[0][:3] + (2, vs[0][4], 1), vs[1][:3] + (2, vs[1][4], 1), vs[0][:3] + (1, vs[0][4], 1), vs[0][:3] + (2, vs[0][4], 0)]
-    # DP = 3 / 2: interior descriptors also held in registers for the whole kernel
-    vs += [vs[0][:3] + (2, vs[0][4], 3), vs[0][:3] + (2, vs[0][4], 2)]
+    # (r29: holding the point-independent interior descriptors in registers for the whole kernel measured
+    # 1-5 % slower at n = 3..5 and was dropped)
     # r28 sweep: register prefetch of the momenta +1.6 % at n = 3; with the descriptor prefetch +2 % at n = 4
-    promote = {4: len(vs) - 3, 5: len(vs) - 6}.get(plan.N)
+    promote = {4: len(vs) - 1, 5: len(vs) - 4}.get(plan.N)
     if promote is not None:
         vs = [vs[promote]] + vs[:promote] + vs[promote + 1:]
     return vs
@@ -84,33 +84,19 @@ def emit_plan_namespace(plan: Plan, ns: str) -> str:
     """Task tables + traits struct T of one lowered plan, in namespace `ns`."""
     N, L = plan.N, plan.layout
     in_flat, out_flat, lines = [], [], []
-    id_fields, id_ld, id_ex = [], [], []
-
-    def _id(cnt, off, tbl, kid):
-        f = f"d{len(id_fields)}"
-        id_fields.append(f"ushort4 {f}[{(cnt + plan.G - 1) // plan.G}];")
-        id_ld.append(f"    qed::load_tasks<T, {cnt}, {off}>(d.{f}, g, {tbl});")
-        id_ex.append(f"    qed::exec_tasks<T, {cnt}, qed::TaskFn<T, {kid}>, {off}>(base, g, d.{f}, qed::TaskFn<T, {kid}>{{}});")
-
     for lv in range(max(len(plan.in_levels), len(plan.out_levels))):
         if lv < len(plan.in_levels):
             t = plan.in_levels[lv]
             lines.append(f"    qed::run_tasks<T, {len(t)}>(base, g, k_in_tasks + {len(in_flat)}, qed::TaskFn<T, 0>{{}});")
-            _id(len(t), 0, f"k_in_tasks + {len(in_flat)}", 0)
             in_flat += t
         if lv < len(plan.out_levels):
             t = plan.out_levels[lv]
             off = lane_offset(len(plan.in_levels[lv]), plan.G) if lv < len(plan.in_levels) else 0
             lines.append(f"    qed::run_tasks<T, {len(t)}, qed::TaskFn<T, 1>, {off}>(base, g, k_out_tasks + {len(out_flat)}, "
                          "qed::TaskFn<T, 1>{});")
-            _id(len(t), off, f"k_out_tasks + {len(out_flat)}", 1)
             out_flat += t
         lines.append("    qed::group_sync<T>(pb);")
-        id_ex.append("    qed::group_sync<T>(pb);")
     interiors = "\n".join(lines) if lines else "    (void)base; (void)g; (void)pb;"
-    id_struct = " ".join(id_fields) if id_fields else "int unused;"
-    load_id = "\n".join(id_ld) if id_ld else "    (void)d; (void)g;"
-    run_id = "\n".join(id_ex) if id_ex else "    (void)base; (void)g; (void)pb; (void)d;"
     struct = [[(k, len(t)) for k, t in st] for st in plan.set_stages[0]]
     per_set = sum(c for st in struct for _, c in st)
     set_flat = []
@@ -182,14 +168,6 @@ struct T {{
   }}
   static __device__ __forceinline__ void run_set_d(double* base, int g, int pb, const SD& d) {{
 {run_set_d}
-  }}
-  // interior-level descriptors are the same for every point: loaded once per kernel into registers (DP & 2)
-  struct ID {{ {id_struct} }};
-  static __device__ __forceinline__ void load_interiors(ID& d, int g) {{
-{load_id}
-  }}
-  static __device__ __forceinline__ void run_interiors_d(double* base, int g, int pb, const ID& d) {{
-{run_id}
   }}
 }};
 

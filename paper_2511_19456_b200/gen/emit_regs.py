@@ -210,7 +210,7 @@ def emit_regs_body1(N: int) -> str:
     return "\n".join(L) + "\n"
 
 
-def emit_regs_body1p(N: int, fence: bool = True) -> str:
+def emit_regs_body1p(N: int, fence: bool = True, inter: bool = False) -> str:
     """N = 3 body with ONE thread per point, in two passes over the outgoing-electron spin s'.
     The thread's 12 phi leaves go to a private shared-memory slot (no exchange, no sharing); each pass
     walks the out-side trie of u-bar(p', s') depth first with the 32 amplitudes of that s' in registers
@@ -220,6 +220,8 @@ def emit_regs_body1p(N: int, fence: bool = True) -> str:
     L = []
     w = L.append
     fn = "regs_body1p_N3" if fence else "regs_body1q_N3"
+    if inter:
+        fn = "regs_body1pi_N3"
     w(f"// ---- generated straight-line body, N = 3 (thread = point, two passes over s'), j = 1")
     w("template <class ARGS, class FIN>")
     w(f"__device__ __forceinline__ void {fn}(const double* __restrict__ mom, long long n, long long pt,")
@@ -281,6 +283,16 @@ def emit_regs_body1p(N: int, fence: bool = True) -> str:
                     w("        __syncwarp();  // scheduling fence: keeps ptxas from hoisting every phi load")
                 w(f"        const qed::spinor l0 = qed::eslash_row(e[{c}][0], I);")
                 w(f"        const qed::spinor l1 = qed::eslash_row_t(e[{c}][1], I);")
+                if inter:
+                    w("        qed::spinor ph[4];")
+                    w("        #pragma unroll")
+                    w(f"        for (int k = 0; k < 4; ++k) ph[k] = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
+                    w("        int ix[8];")
+                    w("        #pragma unroll")
+                    w(f"        for (int k = 0; k < 4; ++k) {{ ix[k] = (k >> 1) | ((k & 1) << {1 + a_}) | ({lb} << {1 + b}); ix[4 + k] = ix[k] | {1 << (1 + c)}; }}")
+                    w("        qed::cdot8_acc(l0, l1, ph, ix, acc);")
+                    w("      }")
+                    continue
                 w("        #pragma unroll")
                 w("        for (int k = 0; k < 4; ++k) {")
                 w(f"          const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
@@ -439,7 +451,8 @@ def emit_regs_source(N: int) -> str:
         f"                                      : (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::V{i}, false>;"
         for i, (d, w, m, p) in enumerate(vs))
     tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "1" if d.startswith("T1") else "2" for d, *_ in vs) + "}"
-    body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) + "\n" + emit_regs_body1p(N) if N == 3 else ""
+    body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) + "\n" + emit_regs_body1p(N) + "\n" + \
+        emit_regs_body1p(N, inter=True) if N == 3 else ""
     t4 = f"""
 // four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
 struct T4 {{
@@ -470,6 +483,14 @@ struct T1P {{
     regs_body1p_N{N}(mom, n, pt, sl, a, fin);
   }}
   static __device__ __forceinline__ unsigned config_of(int idx, int sub) {{ return idx | ((unsigned)sub << (N + 1)); }}
+}};
+// T1P with each out-side block's 8 joins issued interleaved (T1PI)
+struct T1PI : T1P {{
+  template <class ARGS2, class FIN>
+  static __device__ __forceinline__ void body_passes(const double* mom, long long n, long long pt, double* sl,
+                                                     const ARGS2& a, FIN&& fin) {{
+    regs_body1pi_N{N}(mom, n, pt, sl, a, fin);
+  }}
 }};""" if N == 3 else ""
     if N == 2:
         body4 = emit_regs_body1(N)
@@ -535,9 +556,10 @@ def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
     Variant 0 = best of the latest sweep (profiles/sweep_*.jsonl)."""
     if N == 3:
         # r20 sweep: the interleaved join body TI >= T at n = 2 once the transverse vertices shortened T
-        # r28 sweep: one thread per point in two s' passes (T1P) 2.31e9 pts/s (62.5 %) vs 2.01e9 for TI
-        return [("T1P", 8, 1, 1), ("T1P", 8, 1, 0), ("T1P", 4, 2, 1), ("TI", 4, 1, 2), ("T", 4, 1, 2), ("T", 4, 1, 1),
-                ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
+        # r28 sweep: one thread per point in two s' passes (T1P) 2.31e9 pts/s (62.5 %) vs 2.01e9 for TI;
+        # r30: interleaved joins (T1PI) +1.1 %, one fence per tau_1 block (T1PJ) +0.3 % (dropped)
+        return [("T1PI", 8, 1, 1), ("T1P", 8, 1, 1), ("T1P", 8, 1, 0), ("T1P", 4, 2, 1), ("TI", 4, 1, 2), ("T", 4, 1, 2),
+                ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
     # t1 sweep: one thread per point (T1) 1.19e10 pts/s (68 % of FP64 peak) vs 8.18e9 for T
     return [("T1", 8, 1, 2), ("T1", 4, 2, 2), ("T1", 2, 4, 2), ("T1", 4, 2, 1), ("T", 2, 6, 2), ("T", 4, 1, 0),
             ("T", 4, 1, 1), ("T", 2, 6, 1), ("T", 4, 1, 2)]
