@@ -108,6 +108,15 @@ __device__ __forceinline__ void ld_stream_mask(const double* p, double (&m)[5]) 
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(m[4]) : "r"(addr + 32));
 }
 
+// a += b (Berends-Giele current sums)
+__device__ __forceinline__ void add_to(spinor& a, const spinor& b) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    a.v[c].r += b.v[c].r;
+    a.v[c].i += b.v[c].i;
+  }
+}
+
 // acc += sum_c a[c] b[c]  (S2 join: 4 complex multiply-accumulates, 16 DFMA)
 __device__ __forceinline__ void cdot_acc(const spinor& a, const spinor& b, double& re, double& im) {
 #pragma unroll

@@ -75,6 +75,9 @@ const void* qedregs_kernel_N3(int, int);
 int qedregs_num_variants_N3(void);
 void qedregs_config_N2(int, int*, int*, long long*, long long*);
 void qedregs_config_N3(int, int*, int*, long long*, long long*);
+const void* qedregsbg_kernel_N3(int, int);
+int qedregsbg_num_variants_N3(void);
+void qedregsbg_config_N3(int, int*, int*, long long*, long long*);
 }
 
 namespace {
@@ -235,10 +238,14 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   const KernelEntry& ke = algorithm == QED_ALGO_BERENDS_GIELE ? kBGKernels[N - 2] : kKernels[N - 2];
   // n = 1, 2: register-resident straight-line kernels (qed_eval_regs.cuh); n >= 3: lane-group
   // kernels with shared-memory trie staging (qed_eval_kernel.cuh).  QED_KERNEL=group forces the latter.
+  // At n = 1 the Berends-Giele rewrite is the identity (every photon subset of one side has a single
+  // ordering: J_in({a}) = S(Q_a) epsslash_a u, K_out({b}) = ubar epsslash_b), so it runs the same kernel.
   const char* force = getenv("QED_KERNEL");
-  const bool use_regs = algorithm == QED_ALGO_CDAG && N <= 3 && !(force && strcmp(force, "group") == 0);
+  // At n = 2 the Berends-Giele currents have their own register body (qedregsbg_*).
+  const bool use_regs = N <= 3 && !(force && strcmp(force, "group") == 0);
+  const bool bg_regs = algorithm == QED_ALGO_BERENDS_GIELE && N == 3;
   if (use_regs) {
-    const int nv = N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3();
+    const int nv = bg_regs ? qedregsbg_num_variants_N3() : N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3();
     if (options && options->variant >= nv) {
       delete P;
       return fail(QED_ERR_INVALID_ARGUMENT, "options.variant " + std::to_string(options->variant) + " >= " + std::to_string(nv));
@@ -246,9 +253,9 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
     const int v = (options && options->variant >= 0) ? options->variant : variant_from_env(nv);
     P->variant = v;
     P->n_variants = nv;
-    P->kern[0] = N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
-    P->kern[1] = N == 2 ? qedregs_kernel_N2(1, v) : qedregs_kernel_N3(1, v);
-    (N == 2 ? qedregs_config_N2 : qedregs_config_N3)(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
+    P->kern[0] = bg_regs ? qedregsbg_kernel_N3(0, v) : N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
+    P->kern[1] = bg_regs ? qedregsbg_kernel_N3(1, v) : N == 2 ? qedregs_kernel_N2(1, v) : qedregs_kernel_N3(1, v);
+    (bg_regs ? qedregsbg_config_N3 : N == 2 ? qedregs_config_N2 : qedregs_config_N3)(v, &P->wpb, &P->ppw, &P->smem, &P->flops);
   } else {
     const int nv = ke.num_variants();
     if (options && options->variant >= nv) {

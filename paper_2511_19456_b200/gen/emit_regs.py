@@ -308,6 +308,115 @@ def emit_regs_body1p(N: int, fence: bool = True, inter: bool = False) -> str:
     return "\n".join(L) + "\n"
 
 
+def bg_flops(N: int = 3) -> dict:
+    """Algorithmic flops per point of the Berends-Giele register body (emit_regs_body_bg): every current
+    once.  K_out({b, c}) = P_out({b}) epsslash_c + P_out({c}) epsslash_b costs two vertices and 8 adds."""
+    assert N == 3
+    V2 = FLOPS["V"] + FLOPS["V_T"]
+    H = 1 << (N + 2)
+    return {
+        "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
+        "propagator_constants": 2 * N * FLOPS["MASK"],
+        "currents_in": 6 * V2 + 12 * FLOPS["S"],            # J_in({a})[s][lam]
+        "currents_out": 6 * V2 + 12 * FLOPS["S"],           # P_out({b})[s'][lam]
+        "k_sums": 2 * 3 * (2 * 2 * V2 + 4 * 8),             # K_out(A^c)[s'][lam_b][lam_c]
+        "join": 2 * 3 * 4 * 4 * FLOPS["JOIN"],              # one join per subset {a} and configuration
+        "msq": H * FLOPS["ABS2"],
+    }
+
+
+def emit_regs_body_bg(N: int = 3) -> str:
+    """Berends-Giele rewrite (DESIGN.md kernel 2b) of the N = 3 body, one thread per point,
+    two passes over s'.  j = 1: M = sum_a K_out({b, c}) . J_in({a}), J_in({a}) = S(Q_a) epsslash_a u (the phi
+    leaves, private shared-memory slot as in T1P), P_out({x}) = ubar epsslash_x S(Q_{all \\ x}) and
+    K_out({b, c}) = P_out({b}) epsslash_c + P_out({c}) epsslash_b: one join per subset instead of two.
+    P_out(1) is recomputed once per pass (two of the three P_out pairs are held in registers at a time)."""
+    assert N == 3
+    L = []
+    w = L.append
+    w("// ---- generated straight-line body, N = 3, Berends-Giele currents (thread = point, two passes over s'), j = 1")
+    w("template <class ARGS, class FIN>")
+    w("__device__ __forceinline__ void regs_body_bg_N3(const double* __restrict__ mom, long long n, long long pt,")
+    w("                                                double* __restrict__ sl, const ARGS& a, FIN&& fin) {")
+    w("  const int e_out = a.e_out_particle;")
+    w("  double pe[4], pp[4], q[3][4], sg[3];")
+    w("  for (int mu = 0; mu < 4; ++mu) {")
+    w("    pe[mu] = qed::ld_mom(mom + (long long)mu * n + pt);")
+    w("    pp[mu] = qed::ld_mom(mom + (long long)(4 * e_out + mu) * n + pt);")
+    w("  }")
+    w("  for (int i = 0; i < 3; ++i) {")
+    w("    const int pj = (a.photon_particle >> (4 * i)) & 15;")
+    w("    sg[i] = i < a.n_in_ph ? 1.0 : -1.0;")
+    w("    for (int mu = 0; mu < 4; ++mu) q[i][mu] = qed::ld_mom(mom + (long long)(4 * pj + mu) * n + pt);")
+    w("  }")
+    w("  double e[3][2][3];")
+    w("  for (int i = 0; i < 3; ++i) {")
+    w("    double ct, st, cf, sf;")
+    w("    qed::eps_consts(q[i], ct, st, cf, sf);")
+    w("    e[i][0][0] = ct * cf; e[i][0][1] = ct * sf; e[i][0][2] = -st;")
+    w("    e[i][1][0] = -sf; e[i][1][1] = cf; e[i][1][2] = 0.0;")
+    w("  }")
+    w("  // J_in({a})[s][lam] = S(Q_a) epsslash_a(lam) u(p, s) -> private slot, spinor a * 4 + s * 2 + lam")
+    w("  {")
+    w("    const qed::spinor u0 = qed::u_spinor(pe, 0), u1 = qed::u_spinor(pe, 1);")
+    for a_ in range(3):
+        w(f"    {{ double m[5]; qed::mask_regs(pe, q[{a_}], sg[{a_}], m);")
+        for s_, us in ((0, "u0"), (1, "u1")):
+            for lam in range(2):
+                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::prop_col(m, qed::eslash_col{T_[lam]}(e[{a_}][{lam}], {us})));")
+        w("    }")
+    w("  }")
+    w("  double mc[3][5];   // S(Q_{all \\ x})")
+    w("  for (int x = 0; x < 3; ++x) {")
+    w("    double Q0 = pe[0], Q1 = pe[1], Q2 = pe[2], Q3 = pe[3];")
+    w("    for (int i = 0; i < 3; ++i)")
+    w("      if (i != x) { Q0 = fma(sg[i], q[i][0], Q0); Q1 = fma(sg[i], q[i][1], Q1); Q2 = fma(sg[i], q[i][2], Q2); Q3 = fma(sg[i], q[i][3], Q3); }")
+    w("    const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;")
+    w("    const double inv = 1.0 / D;")
+    w("    mc[x][0] = (Q0 + 1.0) * inv; mc[x][1] = (1.0 - Q0) * inv; mc[x][2] = Q1 * inv; mc[x][3] = Q2 * inv; mc[x][4] = Q3 * inv;")
+    w("  }")
+    w("  #pragma unroll 1")
+    w("  for (int sp = 0; sp < 2; ++sp) {")
+    w("    double acc[32];")
+    w("    #pragma unroll")
+    w("    for (int i = 0; i < 32; ++i) acc[i] = 0.0;")
+    w("    const qed::spinor ub = qed::ubar_spinor(pp, sp);")
+    w("    qed::spinor P[3][2];   // P_out({x})[lam_x] (two of the three held at a time)")
+
+    def pout(x):
+        for lam in range(2):
+            w(f"    P[{x}][{lam}] = qed::prop_row(mc[{x}], qed::eslash_row{T_[lam]}(e[{x}][{lam}], ub));")
+
+    def block(a_, b, c):
+        w(f"    {{  // subset {{{a_}}}: K_out({{{b}, {c}}}) . J_in({{{a_}}})")
+        for lb in range(2):
+            w(f"      {{ __syncwarp();  // scheduling fence: keeps ptxas from hoisting every J_in load")
+            w(f"        qed::spinor K0 = qed::eslash_row(e[{c}][0], P[{b}][{lb}]), K1 = qed::eslash_row_t(e[{c}][1], P[{b}][{lb}]);")
+            w(f"        qed::add_to(K0, qed::eslash_row{T_[lb]}(e[{b}][{lb}], P[{c}][0]));")
+            w(f"        qed::add_to(K1, qed::eslash_row{T_[lb]}(e[{b}][{lb}], P[{c}][1]));")
+            w("        #pragma unroll")
+            w("        for (int k = 0; k < 4; ++k) {")
+            w(f"          const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
+            w(f"          const int i0 = (k >> 1) | ((k & 1) << {1 + a_}) | ({lb} << {1 + b});")
+            w("          qed::cdot_acc(K0, ph, acc[2 * i0], acc[2 * i0 + 1]);")
+            w(f"          qed::cdot_acc(K1, ph, acc[2 * (i0 | {1 << (1 + c)})], acc[2 * (i0 | {1 << (1 + c)}) + 1]);")
+            w("        }")
+            w("      }")
+        w("    }")
+
+    pout(1)
+    pout(2)
+    block(0, 1, 2)
+    pout(0)
+    block(1, 0, 2)
+    pout(1)   # recomputed (P_out({1}) was dropped for P_out({0}))
+    block(2, 0, 1)
+    w("    fin(acc, sp);")
+    w("  }")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
 def emit_regs_body4(N: int) -> str:
     """N = 3 body with four threads per point: thread = (point, s', lam_0).  Photon 0's polarisation
     is fixed per thread, so out-side nodes that do not involve photon 0 are computed by both lam_0
@@ -452,7 +561,7 @@ def emit_regs_source(N: int) -> str:
         for i, (d, w, m, p) in enumerate(vs))
     tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "1" if d.startswith("T1") else "2" for d, *_ in vs) + "}"
     body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) + "\n" + emit_regs_body1p(N) + "\n" + \
-        emit_regs_body1p(N, inter=True) if N == 3 else ""
+        emit_regs_body1p(N, inter=True) + "\n" + emit_regs_body_bg(N) if N == 3 else ""
     t4 = f"""
 // four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
 struct T4 {{
@@ -484,6 +593,15 @@ struct T1P {{
   }}
   static __device__ __forceinline__ unsigned config_of(int idx, int sub) {{ return idx | ((unsigned)sub << (N + 1)); }}
 }};
+// Berends-Giele currents, one thread per point, two passes over s' (QED_ALGO_BERENDS_GIELE at n = 2)
+struct T1B : T1P {{
+  static constexpr long long FLOPS_PER_POINT = {sum(bg_flops(N).values()) if N == 3 else 0}LL;
+  template <class ARGS2, class FIN>
+  static __device__ __forceinline__ void body_passes(const double* mom, long long n, long long pt, double* sl,
+                                                     const ARGS2& a, FIN&& fin) {{
+    regs_body_bg_N{N}(mom, n, pt, sl, a, fin);
+  }}
+}};
 // T1P with each out-side block's 8 joins issued interleaved (T1PI)
 struct T1PI : T1P {{
   template <class ARGS2, class FIN>
@@ -505,6 +623,32 @@ struct T1 {{
   }}
   static __device__ __forceinline__ unsigned config_of(int idx, int) {{ return idx; }}
 }};"""
+    bg_c = ""
+    if N == 3:
+        # Berends-Giele variants; r32 sweep: 2.91e9 pts/s without the L2 prefetch, 2.81e9 with it
+        bvs = [("T1B", 8, 1, 0), ("T1B", 8, 1, 1), ("T1B", 4, 2, 1)]
+        variant_structs += "".join(
+            f"struct B{i} {{ static constexpr int WPB = {w_}, MIN_BLOCKS = {m}, PF = {p_}; }};\n" for i, (d, w_, m, p_) in enumerate(bvs))
+        bcases = "\n".join(
+            f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::B{i}, true>\n"
+            f"                                      : (const void*)qed::qed_regs_kernel<{ns}::{d}, {ns}::B{i}, false>;"
+            for i, (d, *_) in enumerate(bvs))
+        bg_c = f"""// Berends-Giele rewrite in registers (one thread per point)
+int qedregsbg_num_variants_N{N}(void) {{ return {len(bvs)}; }}
+const void* qedregsbg_kernel_N{N}(int per_config, int variant) {{
+  switch (variant) {{
+{bcases}
+  }}
+}}
+void qedregsbg_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, long long* smem_per_block,
+                           long long* flops_per_point) {{
+  static const int wpb[{len(bvs)}] = {{{", ".join(str(v[1]) for v in bvs)}}};
+  *warps_per_block = wpb[variant];
+  *points_per_warp = 32;
+  *smem_per_block = (long long)wpb[variant] * 32 * {ns}::T1B::STRIDE * 8;
+  *flops_per_point = {ns}::T1B::FLOPS_PER_POINT;
+}}
+"""
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_regs.py -- do not edit.
 // Register-resident kernel for N = {N} photons (n = {N - 1}); thread = (point, s') [T] or (point, s', lam_0) [T4].
 // Algorithmic FP64 flops per point:
@@ -547,7 +691,7 @@ void qedregs_config_N{N}(int variant, int* warps_per_block, int* points_per_warp
                     (pf[variant] == 2 ? (long long)wpb[variant] * 2 * {4 * (N + 2)} * (32 / tpp[variant]) * 8 : 0);
   *flops_per_point = {ns}::T::FLOPS_PER_POINT;
 }}
-}}
+{bg_c}}}
 """
 
 
