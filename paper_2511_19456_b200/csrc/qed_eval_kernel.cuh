@@ -266,8 +266,7 @@ __device__ __forceinline__ void stage_externals(double* base, int g, const QedEv
 // cannot hoist every leaf load of the subset (which spills).
 // hh: packed (2 swz(hi), 2 swz(hi + 1), 2 swz(ho), 2 swz(ho + 1)) of this lane and subset (gen tables)
 // SB > 1: SB sigma rows of phi stay in registers across the tau loop (1/SB of the ubar reloads)
-// TU: next tau's u-bar loads issued ahead (register double buffer) so their latency overlaps this tau's MACs
-template <class T, int AS, int SB, int TU = 0>
+template <class T, int AS, int SB>
 __device__ __forceinline__ void join_set_sb(const double* __restrict__ base, int h0, int h1, int o0, int o1,
                                             double (&acc)[AS][8]) {
   static_assert(T::NSIG % SB == 0, "sigma blocking must divide NSIG");
@@ -283,36 +282,14 @@ __device__ __forceinline__ void join_set_sb(const double* __restrict__ base, int
         p1[b][c] = ld2(prow + c * T::NHI * 2 + h1);
       }
     }
-    c2 n0[4], n1[4];
-    if constexpr (TU) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        n0[c] = ld2(base + T::UBL + c * T::NHO * 2 + o0);
-        n1[c] = ld2(base + T::UBL + c * T::NHO * 2 + o1);
-      }
-    }
 #pragma unroll 1
     for (int tu = 0; tu < T::NTAU; ++tu) {
       const double* urow = base + T::UBL + tu * 4 * T::NHO * 2;
       c2 u0[4], u1[4];
-      if constexpr (TU) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          u0[c] = n0[c];
-          u1[c] = n1[c];
-        }
-        const double* nrow = base + T::UBL + (tu + 1 < T::NTAU ? tu + 1 : tu) * 4 * T::NHO * 2;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          n0[c] = ld2(nrow + c * T::NHO * 2 + o0);
-          n1[c] = ld2(nrow + c * T::NHO * 2 + o1);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          u0[c] = ld2(urow + c * T::NHO * 2 + o0);
-          u1[c] = ld2(urow + c * T::NHO * 2 + o1);
-        }
+      for (int c = 0; c < 4; ++c) {
+        u0[c] = ld2(urow + c * T::NHO * 2 + o0);
+        u1[c] = ld2(urow + c * T::NHO * 2 + o1);
       }
 #pragma unroll
       for (int b = 0; b < SB; ++b)
@@ -332,12 +309,12 @@ __device__ __forceinline__ void join_set_sb(const double* __restrict__ base, int
   }
 }
 
-template <class T, int AS, int SB = 1, int TU = 0>
+template <class T, int AS, int SB = 1>
 __device__ __forceinline__ void join_set(const double* __restrict__ base, unsigned hh, double (&acc)[AS][8], int lb = 0) {
   const int h0 = hh & 255, h1 = (hh >> 8) & 255, o0 = (hh >> 16) & 255, o1 = hh >> 24;
   base += lb * T::LEAFB;   // leaf buffer of the lb-th subset of a batch (T::SETB subsets per stage)
   if constexpr (SB > 1) {
-    join_set_sb<T, AS, SB, TU>(base, h0, h1, o0, o1, acc);
+    join_set_sb<T, AS, SB>(base, h0, h1, o0, o1, acc);
     return;
   }
 #pragma unroll 1
@@ -421,8 +398,7 @@ struct dp_of<V, decltype(void(V::DP))> {
   static constexpr int value = V::DP;
 };
 
-// DP bit 0: leaf-stage descriptors loaded one subset ahead (T::SD / load_set / run_set_d);
-// bit 1: u-bar rows of the next tau prefetched in the sigma-blocked join (join_set_sb TU)
+// DP: leaf-stage descriptors loaded one subset ahead (T::SD / load_set / run_set_d)
 template <class T, int AS = 2, int SB = 1, int DP = 0>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
@@ -469,7 +445,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
   for (int q = 0; q < AS; ++q)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
-  if constexpr (DP & 1) {
+  if constexpr (DP) {
     // leaf-stage descriptors one subset ahead: subset s0 + 1's are loaded before subset s0's joins
     static_assert(T::SETB == 1, "descriptor prefetch: one subset per leaf stage");
     typename T::SD sd;
@@ -480,7 +456,7 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
       T::run_set_d(base, g, pb, sd);
       group_sync<T>(pb);
       if (s0 + 1 < T::NSETS) T::load_set(sd, g, s0 + 1);
-      join_set<T, AS, SB, (DP & 2)>(base, hh, acc, 0);
+      join_set<T, AS, SB>(base, hh, acc, 0);
       group_sync<T>(pb);
     }
   } else {

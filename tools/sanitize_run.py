@@ -17,7 +17,7 @@ torch.cuda.set_device(0)
 cases = [("cdag", n, 37) for n in (1, 2, 3, 4, 5)] + [("bg", n, 19) for n in (1, 2, 3, 4, 5, 6, 7)] + [("bg", 8, 2)]
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     # racecheck: shared-memory staging of every kernel shape (two-half joins at bg n = 6, 8)
-    cases = [("cdag", 2, 37), ("cdag", 3, 21), ("cdag", 4, 5), ("cdag", 5, 3), ("bg", 5, 3), ("bg", 6, 3),
+    cases = [("cdag", 1, 37), ("cdag", 2, 37), ("bg", 2, 37), ("cdag", 3, 21), ("cdag", 4, 5), ("cdag", 5, 3), ("bg", 5, 3), ("bg", 6, 3),
              ("bg", 7, 2), ("bg", 8, 1)]
 for algo, n, npts in cases:
     mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=5 + n)
