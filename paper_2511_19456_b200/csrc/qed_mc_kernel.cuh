@@ -34,25 +34,49 @@ __device__ __forceinline__ double u53(unsigned hi, unsigned lo) {
   return ((double)r + 0.5) * 0x1.0p-53;
 }
 
-// Massive RAMBO for K final particles (particle 0 = electron, m = 1; others massless),
-// written into mom (particle order e-_in, gamma_in, e-_out, gamma_out...); returns the weight.
-template <int K>
-__device__ double rambo_point(unsigned long long idx, const QedMcArgs& m, double* mom) {
+// RAMBO step 1 for particle i: the isotropic massless momentum q_i (Philox draws 4 i .. 4 i + 3) -> q[4]
+__device__ __forceinline__ void rambo_massless(unsigned long long idx, int i, const QedMcArgs& m, double* q) {
   const uint2 key = make_uint2((unsigned)m.seed, (unsigned)(m.seed >> 32));
+  const uint4 a = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 0u), key);
+  const uint4 b = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 1u), key);
+  const double r1 = u53(a.x, a.y), r2 = u53(a.z, a.w), r3 = u53(b.x, b.y), r4 = u53(b.z, b.w);
+  const double c = 2.0 * r1 - 1.0, st = sqrt(1.0 - c * c), f = 2.0 * M_PI * r2;
+  const double q0 = -log(r3 * r4);
+  double sf, cf;
+  sincos(f, &sf, &cf);
+  q[0] = q0; q[1] = q0 * st * cf; q[2] = q0 * st * sf; q[3] = q0 * c;
+}
+
+// massless K-body volume (2pi)^(4-3K) (pi/2)^(K-1) s^(K-2) / ((K-1)! (K-2)!): one value per launch
+template <int K>
+__device__ double rambo_volume(double s) {
+  double vol = 1.0, fk1 = 1.0, fk2 = 1.0;
+#pragma unroll
+  for (int i = 0; i < K - 1; ++i) vol *= 0.5 * M_PI;
+#pragma unroll
+  for (int i = 0; i < K - 2; ++i) vol *= s;
+#pragma unroll
+  for (int i = 2; i <= K - 1; ++i) fk1 *= i;
+#pragma unroll
+  for (int i = 2; i <= K - 2; ++i) fk2 *= i;
+  vol /= fk1 * fk2;
+  return vol * pow(2.0 * M_PI, 4.0 - 3.0 * K);
+}
+
+// Massive RAMBO for K final particles (particle 0 = electron, m = 1; others massless), steps 2-4, from the
+// massless momenta qin[4 i + mu] (step 1, rambo_massless, one lane per particle), written into mom (particle
+// order e-_in, gamma_in, e-_out, gamma_out...); returns the weight (vol = rambo_volume<K>(s)).
+template <int K>
+__device__ double rambo_point(const double* qin, const QedMcArgs& m, double vol, double* mom) {
   double q[K][4];
   double Q[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const uint4 a = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 0u), key);
-    const uint4 b = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), (unsigned)i, 1u), key);
-    const double r1 = u53(a.x, a.y), r2 = u53(a.z, a.w), r3 = u53(b.x, b.y), r4 = u53(b.z, b.w);
-    const double c = 2.0 * r1 - 1.0, st = sqrt(1.0 - c * c), f = 2.0 * M_PI * r2;
-    const double q0 = -log(r3 * r4);
-    double sf, cf;
-    sincos(f, &sf, &cf);
-    q[i][0] = q0; q[i][1] = q0 * st * cf; q[i][2] = q0 * st * sf; q[i][3] = q0 * c;
 #pragma unroll
-    for (int mu = 0; mu < 4; ++mu) Q[mu] += q[i][mu];
+    for (int mu = 0; mu < 4; ++mu) {
+      q[i][mu] = qin[4 * i + mu];
+      Q[mu] += q[i][mu];
+    }
   }
   const double sqs = m.sqrt_s, s = sqs * sqs;
   const double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
@@ -98,18 +122,6 @@ __device__ double rambo_point(unsigned long long idx, const QedMcArgs& m, double
     prod *= kk / E;
     sum += kk * kk / E;
   }
-  // massless volume (2pi)^(4-3K) (pi/2)^(K-1) s^(K-2) / ((K-1)! (K-2)!)
-  double vol = 1.0, fk1 = 1.0, fk2 = 1.0;
-#pragma unroll
-  for (int i = 0; i < K - 1; ++i) vol *= 0.5 * M_PI;
-#pragma unroll
-  for (int i = 0; i < K - 2; ++i) vol *= s;
-#pragma unroll
-  for (int i = 2; i <= K - 1; ++i) fk1 *= i;
-#pragma unroll
-  for (int i = 2; i <= K - 2; ++i) fk2 *= i;
-  vol /= fk1 * fk2;
-  vol *= pow(2.0 * M_PI, 4.0 - 3.0 * K);
   double xp = 1.0;
 #pragma unroll
   for (int i = 0; i < 2 * K - 3; ++i) xp *= xi;
@@ -128,6 +140,8 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
   double* red = smem + PB * T::STRIDE;    // [PB][3] block reduction scratch
   const unsigned long long lo_all = m.first_index, hi_all = m.first_index + m.n_points;
   const unsigned long long c_begin = lo_all / m.chunk, c_end = (hi_all + m.chunk - 1) / m.chunk;
+  const double vol = rambo_volume<K>(m.sqrt_s * m.sqrt_s);
+  static_assert(K <= G && 4 * K <= 4 * (T::N + 2), "one lane per particle; q staged in the momentum slot");
   for (unsigned long long c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
     const unsigned long long lo = max(lo_all, c * (unsigned long long)m.chunk);
     const unsigned long long hi = min(hi_all, (c + 1) * (unsigned long long)m.chunk);
@@ -137,8 +151,11 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
       const bool valid = idx < hi;
       double w = 0.0;
       bool pass = false;
+      // RAMBO step 1 in parallel (lane i: particle i), steps 2-4 on lane 0 (order of every sum as in the oracle)
+      if (g < K) rambo_massless(valid ? idx : hi - 1, g, m, base + T::MOM + 4 * g);
+      group_sync<T>(pb);
       if (g == 0) {
-        w = rambo_point<K>(valid ? idx : hi - 1, m, base + T::MOM);
+        w = rambo_point<K>(base + T::MOM, m, vol, base + T::MOM);
         pass = true;
         for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
       }

@@ -37,6 +37,8 @@ def emit_bg_source(plan: BGPlan) -> str:
     mb4 = max(1, min(mb, 65536 // (152 * wpb * 32)))
     # r06/r10 sweeps: AS = 4 first unless its register budget costs resident blocks (n >= 7)
     vs = [(wpb, mb4, 4, 1), (wpb, mb, 2, 1)] if mb4 == mb else [(wpb, mb, 2, 1), (wpb, mb4, 4, 1)]
+    # PF = 2: the next point's momenta prefetched into registers (round 2)
+    vs += [v[:3] + (2,) for v in vs]
     lev_flat, lines = [], []
     prev_count, prev_k = 0, None
     for i, (kind, K, tasks) in enumerate(plan.levels):
