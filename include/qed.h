@@ -126,8 +126,10 @@ qed_status qed_eval_msq_host(const qed_process* proc, const double* momenta_host
    n_chunks >= ceil((first_index + n_points) / QED_MC_CHUNK); the caller zeroes it and
    all-reduces it across ranks (the only collective), then sums the
    chunks in index order -- bitwise identical for any split of the index range along
-   chunk boundaries.  Only the north-star direction (in = 1 photon) is supported. */
-#define QED_MC_CHUNK 8192
+   chunk boundaries.  Only the north-star direction (in = 1 photon) is supported.
+   QED_MC_CHUNK is small enough that a 2^24-point call has >= 10 chunks per resident block
+   (load balance of the chunk-per-block kernel). */
+#define QED_MC_CHUNK 1024
 typedef struct {
   double sqrt_s;
   double omega_min;

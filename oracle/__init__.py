@@ -177,7 +177,7 @@ def rambo_point(n_out_ph: int, sqrt_s: float, seed: int, index: int, kind="f64")
 
 
 def mc_sum(n_out_ph: int, sqrt_s: float, omega_min: float, seed: int, first: int, count: int,
-           chunk: int = 8192, threads: int | None = None, kind="f64") -> np.ndarray:
+           chunk: int = 1024, threads: int | None = None, kind="f64") -> np.ndarray:
     """Chunk partial sums [n_chunks, 3] = (sum w|M|^2, sum (w|M|^2)^2, n_pass), n_chunks =
     ceil((first + count) / chunk) (chunks before `first` stay zero)."""
     n_chunks = (first + count + chunk - 1) // chunk

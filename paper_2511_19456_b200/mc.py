@@ -16,9 +16,10 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
-CHUNK = 8192   # = QED_MC_CHUNK (include/qed.h)
+CHUNK = 1024   # = QED_MC_CHUNK (include/qed.h)
 
 
 def n_chunks(n_total: int, chunk: int = CHUNK) -> int:
@@ -45,12 +46,9 @@ def reduce_partials(partials: torch.Tensor, group=None) -> torch.Tensor:
 
 def cross_section(partials: torch.Tensor, n_total: int, sqrt_s: float, n_photons: int) -> dict:
     """sigma and its MC error from the reduced chunk sums (summed in chunk order, on the host)."""
-    p = partials.detach().to("cpu", torch.float64).reshape(-1, 3)
-    s0 = s1 = npass = 0.0
-    for c in range(p.shape[0]):        # fixed order: bitwise reproducible
-        s0 += float(p[c, 0])
-        s1 += float(p[c, 1])
-        npass += float(p[c, 2])
+    p = partials.detach().to("cpu", torch.float64).numpy().reshape(-1, 3)
+    # fixed order, left to right (a running sum: bitwise the sequential loop, for any number of ranks)
+    s0, s1, npass = (float(np.cumsum(p[:, k])[-1]) if p.shape[0] else 0.0 for k in range(3))
     s = sqrt_s * sqrt_s
     norm = 1.0 / (2.0 * (s - 1.0) * math.factorial(n_photons))
     mean = s0 / n_total

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libqed.so")
 
 QED_OK = 0
 QED_SUM = -1
-MC_CHUNK = 8192
+MC_CHUNK = 1024
 _STATUS = {0: "QED_OK", 1: "QED_ERR_INVALID_ARGUMENT", 2: "QED_ERR_UNSUPPORTED", 3: "QED_ERR_CUDA",
            4: "QED_ERR_OUT_OF_MEMORY", 5: "QED_ERR_INTERNAL"}
 
