@@ -158,6 +158,31 @@ struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
   }
 };
 
+// run_tasks8 split in two (BG T::SD / load_set / run_set_d): descriptors into registers ...
+template <class T, int COUNT, int OFF>
+__device__ __forceinline__ void load_tasks8(Desc<T::DW> (&d)[(COUNT + T::G - 1) / T::G], int g, const Desc<T::DW>* __restrict__ tbl) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k) {
+    const int t = gl + k * T::G;
+#pragma unroll
+    for (int w = 0; w < T::DW / 8; ++w) {
+      d[k].v[w] = make_uint4(0, 0, 0, 0);
+      if (t < COUNT) d[k].v[w] = tbl[t].v[w];
+    }
+  }
+}
+// ... and the tasks
+template <class T, int COUNT, class F, int OFF>
+__device__ __forceinline__ void exec_tasks8(double* base, int g, const Desc<T::DW> (&d)[(COUNT + T::G - 1) / T::G], F f) {
+  constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
+  const int gl = (g + T::G - OFF) % T::G;
+#pragma unroll
+  for (int k = 0; k < TRIPS; ++k)
+    if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
+}
+
 // OFF: lane offset, so that two task kinds of one stage occupy different lanes / warps
 template <class T, int COUNT, class F, int OFF = 0>
 __device__ __forceinline__ void run_tasks8(double* base, int g, const Desc<T::DW>* __restrict__ tbl, F f) {
@@ -193,24 +218,28 @@ __device__ __forceinline__ void run_tasks(double* base, int g, const ushort4* __
 }
 
 // run_tasks split in two (T::SD / load_set / run_set_d): descriptors of one task list into registers ...
+// (kept as raw 64-bit words: unpacking them into ushort4 right after the load would wait for it)
 template <class T, int COUNT, int OFF>
-__device__ __forceinline__ void load_tasks(ushort4 (&d)[(COUNT + T::G - 1) / T::G], int g, const ushort4* __restrict__ tbl) {
+__device__ __forceinline__ void load_tasks(uint2 (&d)[(COUNT + T::G - 1) / T::G], int g, const ushort4* __restrict__ tbl) {
   constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
   const int gl = (g + T::G - OFF) % T::G;
+  const uint2* __restrict__ raw = reinterpret_cast<const uint2*>(tbl);
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k) {
     const int t = gl + k * T::G;
-    d[k] = (t < COUNT) ? tbl[t] : make_ushort4(0, 0, 0, 0);
+    d[k] = make_uint2(0u, 0u);
+    if (t < COUNT) d[k] = raw[t];
   }
 }
 // ... and the tasks themselves
 template <class T, int COUNT, class F, int OFF>
-__device__ __forceinline__ void exec_tasks(double* base, int g, const ushort4 (&d)[(COUNT + T::G - 1) / T::G], F f) {
+__device__ __forceinline__ void exec_tasks(double* base, int g, const uint2 (&d)[(COUNT + T::G - 1) / T::G], F f) {
   constexpr int TRIPS = (COUNT + T::G - 1) / T::G;
   const int gl = (g + T::G - OFF) % T::G;
 #pragma unroll
   for (int k = 0; k < TRIPS; ++k)
-    if (COUNT % T::G == 0 || gl + k * T::G < COUNT) f(base, d[k]);
+    if (COUNT % T::G == 0 || gl + k * T::G < COUNT)
+      f(base, make_ushort4(d[k].x & 0xffffu, d[k].x >> 16, d[k].y & 0xffffu, d[k].y >> 16));
 }
 
 template <class T>
@@ -398,7 +427,17 @@ struct dp_of<V, decltype(void(V::DP))> {
   static constexpr int value = V::DP;
 };
 
-// DP: leaf-stage descriptors loaded one subset ahead (T::SD / load_set / run_set_d)
+struct NoSD {};
+template <class T, bool HAS>
+struct sd_of {
+  using type = NoSD;
+};
+template <class T>
+struct sd_of<T, true> {
+  using type = typename T::SD;
+};
+
+// DP: leaf-stage descriptors loaded one subset (batch) ahead (T::SD / load_set / run_set_d)
 template <class T, int AS = 2, int SB = 1, int DP = 0>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
   stage_externals<T>(base, g, a);
@@ -412,13 +451,21 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
     double acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    typename sd_of<T, DP != 0>::type sd;
+    if constexpr (DP) T::load_set(sd, g, 0);
 #pragma unroll 1
     for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
       uint2 ww[T::SETB / 2];   // join offsets: loaded before the leaf stage so their latency overlaps it
 #pragma unroll
       for (int lb = 0; lb < T::SETB; lb += 2) ww[lb / 2] = T::hs_offsets(s0 + lb + q, gh);
-      T::run_set(base, g, pb, s0);
-      group_sync<T>(pb);
+      if constexpr (DP) {
+        T::run_set_d(base, g, pb, sd);
+        group_sync<T>(pb);
+        if (s0 + T::SETB < T::NSETS) T::load_set(sd, g, s0 + T::SETB);
+      } else {
+        T::run_set(base, g, pb, s0);
+        group_sync<T>(pb);
+      }
 #pragma unroll
       for (int lb = 0; lb < T::SETB; lb += 2) {
         const int si = s0 + lb + q;
@@ -446,17 +493,20 @@ __device__ __forceinline__ void eval_point(double* base, int g, int pb, const Qe
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[q][i] = 0.0;
   if constexpr (DP) {
-    // leaf-stage descriptors one subset ahead: subset s0 + 1's are loaded before subset s0's joins
-    static_assert(T::SETB == 1, "descriptor prefetch: one subset per leaf stage");
+    // leaf-stage descriptors one batch ahead: batch s0 + SETB's are loaded before batch s0's joins
     typename T::SD sd;
     T::load_set(sd, g, 0);
 #pragma unroll 1
-    for (int s0 = 0; s0 < T::NSETS; ++s0) {
-      const unsigned hh = T::hiho(s0, g);
+    for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {
+      unsigned hh[T::SETB];
+#pragma unroll
+      for (int lb = 0; lb < T::SETB; ++lb) hh[lb] = T::hiho(s0 + lb, g);
       T::run_set_d(base, g, pb, sd);
       group_sync<T>(pb);
-      if (s0 + 1 < T::NSETS) T::load_set(sd, g, s0 + 1);
-      join_set<T, AS, SB>(base, hh, acc, 0);
+      if (s0 + T::SETB < T::NSETS) T::load_set(sd, g, s0 + T::SETB);
+#pragma unroll
+      for (int lb = 0; lb < T::SETB; ++lb)
+        if (T::NSETS_REAL % T::SETB == 0 || s0 + lb < T::NSETS_REAL) join_set<T, AS, SB>(base, hh[lb], acc, lb);
       group_sync<T>(pb);
     }
   } else {

@@ -121,7 +121,7 @@ def emit_plan_namespace(plan: Plan, ns: str) -> str:
             lines.append(f"    qed::run_tasks<T, {cnt}, qed::TaskFn<T, {kid}>, {lo}>(base, g, "
                          f"k_set_tasks + si * {per_set} + {off}, qed::TaskFn<T, {kid}>{{}});")
             f = f"d{len(sd_fields)}"
-            sd_fields.append(f"ushort4 {f}[{(cnt + plan.G - 1) // plan.G}];")
+            sd_fields.append(f"uint2 {f}[{(cnt + plan.G - 1) // plan.G}];")
             ld_lines.append(f"    qed::load_tasks<T, {cnt}, {lo}>(d.{f}, g, k_set_tasks + si * {per_set} + {off});")
             ex_lines.append(f"    qed::exec_tasks<T, {cnt}, qed::TaskFn<T, {kid}>, {lo}>(base, g, d.{f}, qed::TaskFn<T, {kid}>{{}});")
             off += cnt
