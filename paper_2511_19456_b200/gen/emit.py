@@ -63,11 +63,13 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
     # (r29: holding the point-independent interior descriptors in registers for the whole kernel measured
     # 1-5 % slower at n = 3..5 and was dropped)
     # r28 sweep: register prefetch of the momenta +1.6 % at n = 3; with the descriptor prefetch +2 % at n = 4
-    promote = {4: len(vs) - 1, 5: len(vs) - 4}.get(plan.N)
+    # r40: register prefetch of the momenta +0.7 % at n = 5
+    promote = {4: len(vs) - 1, 5: len(vs) - 4, 6: len(vs) - 1}.get(plan.N)
     if promote is not None:
         vs = [vs[promote]] + vs[:promote] + vs[promote + 1:]
     if plan.N == 4:   # n = 3: sigma blocking at 16 warps/SM (128 registers); r37 sweep: +7 % -> the default
-        vs = [(wpb, min(mb, 4), 2, 2, 2, 0)] + vs + [(wpb, min(mb, 4), 2, 2, 1, 0), (wpb, min(mb, 4), 2, 2, 2, 1)]
+        # r40: + the descriptor prefetch (raw words) +1.4 % -> the default
+        vs = [(wpb, min(mb, 4), 2, 2, 2, 1), (wpb, min(mb, 4), 2, 2, 2, 0)] + vs + [(wpb, min(mb, 4), 2, 2, 1, 0)]
     # (r33: prefetching the next tau's u-bar rows in the sigma-blocked join measured 5 % slower at n = 4: dropped)
     return vs
 
