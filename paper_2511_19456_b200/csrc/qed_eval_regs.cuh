@@ -217,11 +217,16 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
       mpt = lane / TPP;
       buf ^= 1;
     } else if (V::PF == 1) {
-      // L2 prefetch of this warp's next batch of momenta (one row per lane)
+      // L2 prefetch of this warp's next batch of momenta: every 128-byte line of every row (one per lane)
       const long long nx = p0 + warps_total * PPW;
-      if (lane < ROWS && nx < n) {
-        const double* r = a.mom + (long long)lane * n + nx;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+      constexpr int SEG = (PPW * 8 + 127) / 128;   // 128-byte lines per row of the batch
+#pragma unroll
+      for (int e = lane; e < ROWS * SEG; e += 32) {
+        const long long q = nx + (e % SEG) * 16;
+        if (q < n) {
+          const double* r = a.mom + (long long)(e / SEG) * n + q;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+        }
       }
     }
     // amplitudes of NACC configurations -> per-configuration |M|^2 stores, or this thread's part of the sum

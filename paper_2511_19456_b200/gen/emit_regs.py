@@ -702,6 +702,8 @@ def regs_variants(N: int) -> list[tuple[str, int, int, int]]:
         # r20 sweep: the interleaved join body TI >= T at n = 2 once the transverse vertices shortened T
         # r28 sweep: one thread per point in two s' passes (T1P) 2.31e9 pts/s (62.5 %) vs 2.01e9 for TI;
         # r30: interleaved joins (T1PI) +1.1 %, one fence per tau_1 block (T1PJ) +0.3 % (dropped)
+        # r41: the L2 prefetch now covers both 128-byte lines of each 32-point row: +4 % (2.44e9, 66 %);
+        #      an L1 prefetch instead measured the same (+0.3 %, dropped)
         return [("T1PI", 8, 1, 1), ("T1P", 8, 1, 1), ("T1P", 8, 1, 0), ("T1P", 4, 2, 1), ("TI", 4, 1, 2), ("T", 4, 1, 2),
                 ("T", 4, 1, 1), ("T", 4, 1, 0), ("T", 2, 5, 2), ("T4", 4, 4, 1), ("T4", 4, 3, 2), ("TI", 4, 1, 1)]
     # t1 sweep: one thread per point (T1) 1.19e10 pts/s (68 % of FP64 peak) vs 8.18e9 for T
