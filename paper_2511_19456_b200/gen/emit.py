@@ -69,8 +69,8 @@ def variants(plan: Plan) -> list[tuple[int, int, int, int]]:
         vs = [vs[promote]] + vs[:promote] + vs[promote + 1:]
     if plan.N == 4:   # n = 3: sigma blocking at 16 warps/SM (128 registers); r37 sweep: +7 % -> the default
         # r40: + the descriptor prefetch (raw words) +1.4 % -> the default
-        vs = [(wpb, min(mb, 4), 2, 2, 2, 1), (wpb, min(mb, 4), 2, 2, 2, 0)] + vs + [(wpb, min(mb, 4), 2, 2, 1, 0),
-                                                                             (wpb, 3, 4, 2, 2, 1)]
+        # (r43: AS = 4 at 12 warps measured -0.8 %)
+        vs = [(wpb, min(mb, 4), 2, 2, 2, 1), (wpb, min(mb, 4), 2, 2, 2, 0)] + vs + [(wpb, min(mb, 4), 2, 2, 1, 0)]
     # (r33: prefetching the next tau's u-bar rows in the sigma-blocked join measured 5 % slower at n = 4: dropped)
     return vs
 

@@ -189,3 +189,51 @@ def test_bg_join_halves_match_oracle(N, hs):
     for k in range(2):
         B = eval_point_bg(plan, mom[k], 1)
         assert np.max(np.abs(A[k] - B)) <= 1e-12 * np.max(np.abs(A[k]))
+
+
+# ---------------------------------------------------------------- register bodies: flop counts from the emitted code
+_CALL_FLOPS = {"eslash_col(": 40, "eslash_row(": 40, "eslash_col_t(": 24, "eslash_row_t(": 24, "prop_col(": 56,
+               "prop_row(": 56, "cdot_acc(": 32, "cdot8_acc(": 8 * 32, "add_to(": 8}
+
+
+def _count_body_flops(src: str, fn: str) -> int:
+    """Flops of the vertex / propagator / join / sum calls in the straight-line body `fn` of generated source,
+    each weighted by the trip count of the enclosing `for (...; x < K; ...)` loops (read from the text)."""
+    import re
+    body = src[src.index(f"void {fn}("):]
+    body = body[:body.index("\n}\n")]
+    total, stack, pending = 0, [], 1
+    for line in body.split("\n"):
+        m = re.search(r"for \(int \w+ = 0; \w+ < (\d+); \+\+\w+\)", line)
+        mult = 1
+        for k in stack:
+            mult *= k
+        if m:
+            pending = int(m.group(1))
+        for call, fl in _CALL_FLOPS.items():
+            total += mult * (pending if m else 1) * fl * line.count(call)
+        for ch in line:
+            if ch == "{":
+                stack.append(pending if m else 1)
+                m, pending = None, 1
+            elif ch == "}":
+                stack.pop()
+    return total
+
+
+def test_register_body_flops_match_the_flop_model():
+    """The roofline numerator of the register kernels (gen/emit_regs.py _flops / bg_flops) equals what their
+    emitted straight-line bodies call: n = 1 (T1), n = 2 (T1P, and T1PI: the headline kernel's body) and BG n = 2
+    (T1B, whose recomputed P_out({1}) is executed, not algorithmic work)."""
+    from paper_2511_19456_b200.gen.emit_regs import _flops, bg_flops, emit_regs_source
+    for N, fn, model in ((2, "regs_body1_N2", _flops(2)), (3, "regs_body1p_N3", _flops(3)),
+                         (3, "regs_body1pi_N3", _flops(3)), (3, "regs_body_bg_N3", bg_flops(3))):
+        src = emit_regs_source(N)
+        vertex_part = sum(v for k, v in model.items() if k not in ("external", "propagator_constants", "msq"))
+        got = _count_body_flops(src, fn)
+        if fn == "regs_body_bg_N3":
+            got -= 2 * (40 + 24 + 2 * 56)      # P_out({1}) recomputed once per s' pass
+        assert got == vertex_part, (fn, got, vertex_part)
+    # the generic plan minus the transverse-vertex saving (16 flop per eps(k, 2) vertex, half of all vertices)
+    assert sum(_flops(2).values()) == make_plan(2).flops_per_point - 16 * 8
+    assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36
