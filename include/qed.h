@@ -77,6 +77,8 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
    exponential scaling: the sum over the
    orderings of each photon subset is taken inside the propagators (Berends-Giele currents), one join
    per subset.  Same |M|^2 (same oracle), fewer flops: 7.8 k vs 10.7 k (n = 2), 310 k vs 6.2 M (n = 5).
+   At n = 1 the rewrite is the identity (one ordering per subset) and both algorithms run the same kernel;
+   at n = 2 both run one-thread-per-point register kernels, at n >= 3 lane-group kernels.
    variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable; an index
    >= qed_process_info.n_variants is QED_ERR_INVALID_ARGUMENT. */
 typedef enum { QED_ALGO_CDAG = 0, QED_ALGO_BERENDS_GIELE = 1 } qed_algorithm;
