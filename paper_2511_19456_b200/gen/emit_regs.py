@@ -325,7 +325,7 @@ def bg_flops(N: int = 3) -> dict:
     }
 
 
-def emit_regs_body_bg(N: int = 3, msmem: bool = False) -> str:
+def emit_regs_body_bg(N: int = 3) -> str:
     """Berends-Giele rewrite (DESIGN.md kernel 2b) of the N = 3 body, one thread per point,
     two passes over s'.  j = 1: M = sum_a K_out({b, c}) . J_in({a}), J_in({a}) = S(Q_a) epsslash_a u (the phi
     leaves, private shared-memory slot as in T1P), P_out({x}) = ubar epsslash_x S(Q_{all \\ x}) and
@@ -334,11 +334,9 @@ def emit_regs_body_bg(N: int = 3, msmem: bool = False) -> str:
     assert N == 3
     L = []
     w = L.append
-    fname = "regs_body_bgm_N3" if msmem else "regs_body_bg_N3"
-    w("// ---- generated straight-line body, N = 3, Berends-Giele currents (thread = point, two passes over s'), j = 1" +
-      ("; S(Q_{all \\ x}) constants in the slot after the J_in leaves" if msmem else ""))
+    w("// ---- generated straight-line body, N = 3, Berends-Giele currents (thread = point, two passes over s'), j = 1")
     w("template <class ARGS, class FIN>")
-    w(f"__device__ __forceinline__ void {fname}(const double* __restrict__ mom, long long n, long long pt,")
+    w("__device__ __forceinline__ void regs_body_bg_N3(const double* __restrict__ mom, long long n, long long pt,")
     w("                                                double* __restrict__ sl, const ARGS& a, FIN&& fin) {")
     w("  const int e_out = a.e_out_particle;")
     w("  double pe[4], pp[4], q[3][4], sg[3];")
@@ -368,21 +366,14 @@ def emit_regs_body_bg(N: int = 3, msmem: bool = False) -> str:
                 w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::prop_col(m, qed::eslash_col{T_[lam]}(e[{a_}][{lam}], {us})));")
         w("    }")
     w("  }")
-    if not msmem:
-        w("  double mc[3][5];   // S(Q_{all \\ x})")
+    w("  double mc[3][5];   // S(Q_{all \\ x})")
     w("  for (int x = 0; x < 3; ++x) {")
     w("    double Q0 = pe[0], Q1 = pe[1], Q2 = pe[2], Q3 = pe[3];")
     w("    for (int i = 0; i < 3; ++i)")
     w("      if (i != x) { Q0 = fma(sg[i], q[i][0], Q0); Q1 = fma(sg[i], q[i][1], Q1); Q2 = fma(sg[i], q[i][2], Q2); Q3 = fma(sg[i], q[i][3], Q3); }")
     w("    const double D = Q0 * Q0 - Q1 * Q1 - Q2 * Q2 - Q3 * Q3 - 1.0;")
     w("    const double inv = 1.0 / D;")
-    if msmem:
-        w("    double* mx = sl + 96 + 6 * x;")
-        w("    reinterpret_cast<double2*>(mx)[0] = make_double2((Q0 + 1.0) * inv, (1.0 - Q0) * inv);")
-        w("    reinterpret_cast<double2*>(mx)[1] = make_double2(Q1 * inv, Q2 * inv);")
-        w("    mx[4] = Q3 * inv;")
-    else:
-        w("    mc[x][0] = (Q0 + 1.0) * inv; mc[x][1] = (1.0 - Q0) * inv; mc[x][2] = Q1 * inv; mc[x][3] = Q2 * inv; mc[x][4] = Q3 * inv;")
+    w("    mc[x][0] = (Q0 + 1.0) * inv; mc[x][1] = (1.0 - Q0) * inv; mc[x][2] = Q1 * inv; mc[x][3] = Q2 * inv; mc[x][4] = Q3 * inv;")
     w("  }")
     w("  #pragma unroll 1")
     w("  for (int sp = 0; sp < 2; ++sp) {")
@@ -393,12 +384,6 @@ def emit_regs_body_bg(N: int = 3, msmem: bool = False) -> str:
     w("    qed::spinor P[3][2];   // P_out({x})[lam_x] (two of the three held at a time)")
 
     def pout(x):
-        if msmem:
-            w(f"    {{ double m[5]; qed::ld_stream_mask(sl + {96 + 6 * x}, m);")
-            for lam in range(2):
-                w(f"      P[{x}][{lam}] = qed::prop_row(m, qed::eslash_row{T_[lam]}(e[{x}][{lam}], ub));")
-            w("    }")
-            return
         for lam in range(2):
             w(f"    P[{x}][{lam}] = qed::prop_row(mc[{x}], qed::eslash_row{T_[lam]}(e[{x}][{lam}], ub));")
 
@@ -576,7 +561,7 @@ def emit_regs_source(N: int) -> str:
         for i, (d, w, m, p) in enumerate(vs))
     tpp = "{" + ", ".join("4" if d in ("T4", "TH") else "1" if d.startswith("T1") else "2" for d, *_ in vs) + "}"
     body4 = emit_regs_body4(N) + "\n" + emit_regs_body_interleaved(N) + "\n" + emit_regs_body1p(N) + "\n" + \
-        emit_regs_body1p(N, inter=True) + "\n" + emit_regs_body_bg(N) + "\n" + emit_regs_body_bg(N, msmem=True) if N == 3 else ""
+        emit_regs_body1p(N, inter=True) + "\n" + emit_regs_body_bg(N) if N == 3 else ""
     t4 = f"""
 // four threads per point: (point, s', lam_0); accumulators s | lam_1 << 1 | lam_2 << 2
 struct T4 {{
@@ -617,15 +602,6 @@ struct T1B : T1P {{
     regs_body_bg_N{N}(mom, n, pt, sl, a, fin);
   }}
 }};
-// T1B with the propagator constants of the complements of {{x}} in the private slot (48 instead of 72 spilled bytes; 7 warps/SM)
-struct T1BM : T1B {{
-  static constexpr int STRIDE = 114;
-  template <class ARGS2, class FIN>
-  static __device__ __forceinline__ void body_passes(const double* mom, long long n, long long pt, double* sl,
-                                                     const ARGS2& a, FIN&& fin) {{
-    regs_body_bgm_N{N}(mom, n, pt, sl, a, fin);
-  }}
-}};
 // T1P with each out-side block's 8 joins issued interleaved (T1PI)
 struct T1PI : T1P {{
   template <class ARGS2, class FIN>
@@ -651,7 +627,7 @@ struct T1 {{
     if N == 3:
         # Berends-Giele variants; r32 sweep: 2.91e9 pts/s without the L2 prefetch, 2.81e9 with it
         # (r44: moving the complement propagator constants to the private slot, at 7 warps/SM, measured -12 %)
-        bvs = [("T1B", 8, 1, 0), ("T1B", 8, 1, 1), ("T1B", 4, 2, 1), ("T1BM", 7, 1, 0), ("T1BM", 7, 1, 1)]
+        bvs = [("T1B", 8, 1, 0), ("T1B", 8, 1, 1), ("T1B", 4, 2, 1)]
         variant_structs += "".join(
             f"struct B{i} {{ static constexpr int WPB = {w_}, MIN_BLOCKS = {m}, PF = {p_}; }};\n" for i, (d, w_, m, p_) in enumerate(bvs))
         bcases = "\n".join(
@@ -670,8 +646,7 @@ void qedregsbg_config_N{N}(int variant, int* warps_per_block, int* points_per_wa
   static const int wpb[{len(bvs)}] = {{{", ".join(str(v[1]) for v in bvs)}}};
   *warps_per_block = wpb[variant];
   *points_per_warp = 32;
-  static const int stride[{len(bvs)}] = {{{", ".join(f"{ns}::{v[0]}::STRIDE" for v in bvs)}}};
-  *smem_per_block = (long long)wpb[variant] * 32 * stride[variant] * 8;
+  *smem_per_block = (long long)wpb[variant] * 32 * {ns}::T1B::STRIDE * 8;
   *flops_per_point = {ns}::T1B::FLOPS_PER_POINT;
 }}
 """
