@@ -417,7 +417,7 @@ __device__ __forceinline__ void join_set_hs(const double* __restrict__ base, uin
 
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
-// launch-variant field DP (descriptor prefetch, CDAG plans only); variants without it read 0
+// launch-variant field DP (descriptor prefetch; plans that emit T::SD); variants without the field read 0
 template <class V, class = void>
 struct dp_of {
   static constexpr int value = 0;
