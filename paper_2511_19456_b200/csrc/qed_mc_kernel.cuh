@@ -128,6 +128,84 @@ __device__ double rambo_point(const double* qin, const QedMcArgs& m, double vol,
   return vol * xp * sqs * prod / sum;
 }
 
+// The same steps 2-4 spread over the lanes of a group (lane i: particle i; every lane of the group's first warp
+// takes part, lanes >= K shadow particle K - 1).  The per-particle square roots and divisions run in parallel;
+// every sum is gathered with shuffles and accumulated in particle order, as in rambo_point, so all lanes hold the
+// same xi and weight and take the same Newton exit.  mom is written by lane i (particle i) and lane 0 (beams).
+template <int K, int G>
+__device__ double rambo_group(const double* qin, const QedMcArgs& m, double vol, double* mom, int g) {
+  constexpr int GW = G < 32 ? G : 32;                       // lanes of the group inside this warp
+  const int lane = threadIdx.x & 31;
+  const int base = lane & ~(GW - 1);
+  const unsigned mask = GW == 32 ? 0xffffffffu : (((1u << GW) - 1u) << base);
+  const int i = g < K ? g : K - 1;
+  double Q[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) Q[mu] += qin[4 * j + mu];
+  double q[4];
+#pragma unroll
+  for (int mu = 0; mu < 4; ++mu) q[mu] = qin[4 * i + mu];
+  const double sqs = m.sqrt_s, s = sqs * sqs;
+  const double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
+  const double b1 = -Q[1] / M, b2 = -Q[2] / M, b3 = -Q[3] / M;
+  const double x = sqs / M, gam = Q[0] / M, aa = 1.0 / (1.0 + gam);
+  const double bq = b1 * q[1] + b2 * q[2] + b3 * q[3];
+  const double p0 = x * (gam * q[0] + bq);
+  const double pv0 = x * (q[1] + b1 * q[0] + aa * bq * b1);
+  const double pv1 = x * (q[2] + b2 * q[0] + aa * bq * b2);
+  const double pv2 = x * (q[3] + b3 * q[0] + aa * bq * b3);
+  const double mi2 = (i == 0) ? 1.0 : 0.0;
+  double xi = sqrt(1.0 - 1.0 / s);
+  for (int it = 0; it < 50; ++it) {
+    const double e = sqrt(mi2 + xi * xi * p0 * p0);
+    const double d = xi * p0 * p0 / e;
+    double f = -sqs, df = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      f += __shfl_sync(mask, e, base + j);
+      df += __shfl_sync(mask, d, base + j);
+    }
+    const double dxi = f / df;
+    xi -= dxi;
+    if (fabs(dxi) <= 1e-15 * xi) break;
+  }
+  const double kx = xi * pv0, ky = xi * pv1, kz = xi * pv2;
+  const double E = sqrt(mi2 + xi * xi * p0 * p0);
+  const double kk = sqrt(kx * kx + ky * ky + kz * kz);
+  const double r1 = kk / E, r2 = kk * kk / E;
+  double prod = 1.0, sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    prod *= __shfl_sync(mask, r1, base + j);
+    sum += __shfl_sync(mask, r2, base + j);
+  }
+  if (g < K) {
+    double* o = mom + 8 + 4 * g;
+    o[0] = E; o[1] = kx; o[2] = ky; o[3] = kz;
+  }
+  if (g == 0) {
+    const double kin = (s - 1.0) / (2.0 * sqs);
+    mom[0] = (s + 1.0) / (2.0 * sqs); mom[1] = 0.0; mom[2] = 0.0; mom[3] = -kin;
+    mom[4] = kin; mom[5] = 0.0; mom[6] = 0.0; mom[7] = kin;
+  }
+  double xp = 1.0;
+#pragma unroll
+  for (int j = 0; j < 2 * K - 3; ++j) xp *= xi;
+  return vol * xp * sqs * prod / sum;
+}
+
+// launch-variant field MCS: 1 = RAMBO steps 2-4 serially on lane 0 (round-1 form); absent = 0
+template <class V, class = void>
+struct mcs_of {
+  static constexpr int value = 0;
+};
+template <class V>
+struct mcs_of<V, decltype(void(V::MCS))> {
+  static constexpr int value = V::MCS;
+};
+
 template <class T, class V>
 __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
   extern __shared__ __align__(16) double smem[];
@@ -151,15 +229,22 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
       const bool valid = idx < hi;
       double w = 0.0;
       bool pass = false;
-      // RAMBO step 1 in parallel (lane i: particle i), steps 2-4 on lane 0 (order of every sum as in the oracle)
+      // RAMBO: step 1 one lane per particle; steps 2-4 over the group's first warp (rambo_group; every sum in
+      // particle order, as in the oracle) or, with V::MCS, serially on lane 0 (rambo_point)
       if (g < K) rambo_massless(valid ? idx : hi - 1, g, m, base + T::MOM + 4 * g);
       group_sync<T>(pb);
+      if constexpr (mcs_of<V>::value) {
+        if (g == 0) w = rambo_point<K>(base + T::MOM, m, vol, base + T::MOM);
+      } else {
+        // stage-1 momenta are read by every lane before any lane overwrites them: the group's lanes are in one
+        // warp here (G <= 32) or the writers are (G = 64: lanes 0..31), and the shuffles order the reads first
+        if (g < 32) w = rambo_group<K, G>(base + T::MOM, m, vol, base + T::MOM, g);
+      }
+      group_sync<T>(pb);
       if (g == 0) {
-        w = rambo_point<K>(base + T::MOM, m, vol, base + T::MOM);
         pass = true;
         for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
       }
-      group_sync<T>(pb);
       double amp[2 * T::NAMP];
       eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
       const double msq = group_msq<T>(amp, g, pb, base, a);
