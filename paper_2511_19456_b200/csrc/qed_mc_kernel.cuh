@@ -147,6 +147,7 @@ __device__ double rambo_group(const double* qin, const QedMcArgs& m, double vol,
   double q[4];
 #pragma unroll
   for (int mu = 0; mu < 4; ++mu) q[mu] = qin[4 * i + mu];
+  __syncwarp(mask);   // every lane has read the stage-1 momenta before any lane overwrites them (mom aliases qin)
   const double sqs = m.sqrt_s, s = sqs * sqs;
   const double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
   const double b1 = -Q[1] / M, b2 = -Q[2] / M, b3 = -Q[3] / M;
@@ -236,8 +237,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedE
       if constexpr (mcs_of<V>::value) {
         if (g == 0) w = rambo_point<K>(base + T::MOM, m, vol, base + T::MOM);
       } else {
-        // stage-1 momenta are read by every lane before any lane overwrites them: the group's lanes are in one
-        // warp here (G <= 32) or the writers are (G = 64: lanes 0..31), and the shuffles order the reads first
+        // the group's RAMBO lanes are one warp (G <= 32: the group; G = 64: its lanes 0..31)
         if (g < 32) w = rambo_group<K, G>(base + T::MOM, m, vol, base + T::MOM, g);
       }
       group_sync<T>(pb);
