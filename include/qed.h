@@ -26,6 +26,10 @@
  *   - Errors: every function returns a qed_status; qed_last_error() gives a
  *     thread-local message for the last non-OK status.  No exceptions cross the ABI.
  *     A handle is immutable after creation and may be used from several streams/threads.
+ *   - Device binding: a handle belongs to the device that was current when it was
+ *     created.  Every entry point that launches work checks the calling thread's current
+ *     device against it and returns QED_ERR_INVALID_ARGUMENT on a mismatch (it never
+ *     switches devices itself).
  */
 #ifndef QED_H
 #define QED_H
@@ -80,11 +84,17 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
    At n = 1 the rewrite is the identity (one ordering per subset) and both algorithms run the same kernel;
    at n = 2 both run one-thread-per-point register kernels, at n >= 3 lane-group kernels.
    variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable; an index
-   >= qed_process_info.n_variants is QED_ERR_INVALID_ARGUMENT. */
+   >= qed_process_info.n_variants, or a QED_VARIANT that is not such an index, is
+   QED_ERR_INVALID_ARGUMENT (no silent fallback).
+   kernel_family: QED_FAMILY_DEFAULT picks the register kernels at n <= 2 and the lane-group kernels
+   above; QED_FAMILY_LANE_GROUP forces the lane-group kernels at n <= 2 too (comparison runs).
+   No other environment variable changes what the library does. */
 typedef enum { QED_ALGO_CDAG = 0, QED_ALGO_BERENDS_GIELE = 1 } qed_algorithm;
+typedef enum { QED_FAMILY_DEFAULT = 0, QED_FAMILY_LANE_GROUP = 1 } qed_kernel_family;
 typedef struct {
   int algorithm;
   int variant;
+  int kernel_family;
 } qed_process_options;
 qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec* out, int n_photons,
                                  const qed_process_options* options, qed_process** proc);

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
         for (int idx = 0; idx < NACC; ++idx) {
           const unsigned h = T::config_of(idx, sub_);
           const double t = fma(acc[2 * idx], acc[2 * idx], acc[2 * idx + 1] * acc[2 * idx + 1]);
-          sum += ((h & a.fixed_mask) == a.fixed_val) ? t : 0.0;
+          sum += (h != 0xffffffffu && (h & a.fixed_mask) == a.fixed_val) ? t : 0.0;
         }
       }
     };

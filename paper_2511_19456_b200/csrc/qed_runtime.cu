@@ -120,12 +120,25 @@ const KernelEntry kBGKernels[] = {
     {qedbg_kernel_N9, qedbg_mc_kernel_N9, qedbg_config_N9, qedbg_num_variants_N9},
 };
 
-// launch variant from QED_VARIANT (tuning experiments); 0 = default, out-of-range -> 0
+// launch variant from QED_VARIANT (tuning experiments); unset = 0 (default); anything that is not an
+// index in [0, n_variants) is an error (-1), never a silent fallback.
 int variant_from_env(int n_variants) {
   const char* v = getenv("QED_VARIANT");
-  if (!v) return 0;
-  int x = atoi(v);
-  return (x >= 0 && x < n_variants) ? x : 0;
+  if (!v || !*v) return 0;
+  char* end = nullptr;
+  long x = strtol(v, &end, 10);
+  return (end && *end == '\0' && x >= 0 && x < n_variants) ? (int)x : -1;
+}
+
+// every entry point runs on the device the handle was created on (include/qed.h "Device binding")
+qed_status check_device(int device) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (cur != device)
+    return fail(QED_ERR_INVALID_ARGUMENT, "current device " + std::to_string(cur) + " differs from the handle's device " +
+                                              std::to_string(device));
+  return QED_OK;
 }
 
 }  // namespace
@@ -181,6 +194,8 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   if (N != n_photons + 1)
     return fail(QED_ERR_INVALID_ARGUMENT, "in.n_photons + out.n_photons must equal n_photons + 1");
   const int algorithm = options ? options->algorithm : QED_ALGO_CDAG;
+  if (options && options->kernel_family != QED_FAMILY_DEFAULT && options->kernel_family != QED_FAMILY_LANE_GROUP)
+    return fail(QED_ERR_INVALID_ARGUMENT, "unknown kernel_family");
   if (algorithm != QED_ALGO_CDAG && algorithm != QED_ALGO_BERENDS_GIELE)
     return fail(QED_ERR_INVALID_ARGUMENT, "unknown algorithm");
   const int n_max = algorithm == QED_ALGO_BERENDS_GIELE ? 8 : 5;
@@ -240,9 +255,8 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   // kernels with shared-memory trie staging (qed_eval_kernel.cuh).  QED_KERNEL=group forces the latter.
   // At n = 1 the Berends-Giele rewrite is the identity (every photon subset of one side has a single
   // ordering: J_in({a}) = S(Q_a) epsslash_a u, K_out({b}) = ubar epsslash_b), so it runs the same kernel.
-  const char* force = getenv("QED_KERNEL");
   // At n = 2 the Berends-Giele currents have their own register body (qedregsbg_*).
-  const bool use_regs = N <= 3 && !(force && strcmp(force, "group") == 0);
+  const bool use_regs = N <= 3 && !(options && options->kernel_family == QED_FAMILY_LANE_GROUP);
   const bool bg_regs = algorithm == QED_ALGO_BERENDS_GIELE && N == 3;
   if (use_regs) {
     const int nv = bg_regs ? qedregsbg_num_variants_N3() : N == 2 ? qedregs_num_variants_N2() : qedregs_num_variants_N3();
@@ -251,6 +265,10 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
       return fail(QED_ERR_INVALID_ARGUMENT, "options.variant " + std::to_string(options->variant) + " >= " + std::to_string(nv));
     }
     const int v = (options && options->variant >= 0) ? options->variant : variant_from_env(nv);
+    if (v < 0) {
+      delete P;
+      return fail(QED_ERR_INVALID_ARGUMENT, "QED_VARIANT must be an integer in [0, " + std::to_string(nv) + ")");
+    }
     P->variant = v;
     P->n_variants = nv;
     P->kern[0] = bg_regs ? qedregsbg_kernel_N3(0, v) : N == 2 ? qedregs_kernel_N2(0, v) : qedregs_kernel_N3(0, v);
@@ -263,6 +281,10 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
       return fail(QED_ERR_INVALID_ARGUMENT, "options.variant " + std::to_string(options->variant) + " >= " + std::to_string(nv));
     }
     const int v = (options && options->variant >= 0) ? options->variant : variant_from_env(nv);
+    if (v < 0) {
+      delete P;
+      return fail(QED_ERR_INVALID_ARGUMENT, "QED_VARIANT must be an integer in [0, " + std::to_string(nv) + ")");
+    }
     P->variant = v;
     P->n_variants = nv;
     P->kern[0] = ke.kernel(0, v);
@@ -318,6 +340,8 @@ static qed_status launch_eval(const qed_process* P, const double* mom, int64_t n
   if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
   if (n_points == 0) return QED_OK;
   if (!mom || !out) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
+  qed_status dst = check_device(P->device);
+  if (dst != QED_OK) return dst;
   if (((uintptr_t)mom & 7) || ((uintptr_t)out & 7)) return fail(QED_ERR_INVALID_ARGUMENT, "pointers must be 8-byte aligned");
   qed::QedEvalArgs a = P->args;
   a.mom = mom;
@@ -349,8 +373,19 @@ qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_hos
   if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
   if (n_points == 0) return QED_OK;
   if (!momenta_host || !out_host) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
+  qed_status dst = check_device(P->device);
+  if (dst != QED_OK) return dst;
   std::lock_guard<std::mutex> lock(P->mu);
   cudaError_t e;
+  // On any error after the first enqueue, drain both streams before returning, so that no DMA still
+  // targets the caller's host buffers when the call returns (the caller may free them).
+  auto drain = [&](qed_status st) {
+    for (int b = 0; b < 2; ++b)
+      if (P->hstream[b]) cudaStreamSynchronize(P->hstream[b]);
+    return st;
+  };
+  int max_pitch = 0;
+  if (cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, P->device) != cudaSuccess) max_pitch = 0;
   // Pipelined over chunks of points on two streams: chunk c's H2D (a 2D copy of its columns of the
   // SoA rows), kernel and D2H go to stream c % 2 and its staging buffer, so the upload of chunk c+1
   // overlaps the kernel and download of chunk c.  PCIe bound: ~160 B in per point at n = 2.
@@ -381,17 +416,25 @@ qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_hos
     const int b = c & 1;
     const long long cnt = std::min<long long>(chunk, n_points - i0);
     cudaStream_t st = P->hstream[b];
-    e = cudaMemcpy2DAsync(P->d_mom[b], sizeof(double) * (size_t)cnt, momenta_host + i0, sizeof(double) * (size_t)n_points,
-                          sizeof(double) * (size_t)cnt, rows, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    const size_t spitch = sizeof(double) * (size_t)n_points;
+    if (spitch <= (size_t)max_pitch) {
+      e = cudaMemcpy2DAsync(P->d_mom[b], sizeof(double) * (size_t)cnt, momenta_host + i0, spitch,
+                            sizeof(double) * (size_t)cnt, rows, cudaMemcpyHostToDevice, st);
+    } else {   // source pitch above the device limit (~2^28 points): one copy per SoA row
+      e = cudaSuccess;
+      for (int r = 0; r < rows && e == cudaSuccess; ++r)
+        e = cudaMemcpyAsync(P->d_mom[b] + (size_t)r * cnt, momenta_host + (size_t)r * n_points + i0,
+                            sizeof(double) * (size_t)cnt, cudaMemcpyHostToDevice, st);
+    }
+    if (e != cudaSuccess) return drain(cuda_fail(e, "H2D copy"));
     qed_status stt = launch_eval(P, P->d_mom[b], cnt, P->d_out[b], st, 0);
-    if (stt != QED_OK) return stt;
+    if (stt != QED_OK) return drain(stt);
     e = cudaMemcpyAsync(out_host + i0, P->d_out[b], sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    if (e != cudaSuccess) return drain(cuda_fail(e, "D2H copy"));
   }
   for (int b = 0; b < 2; ++b) {
     e = cudaStreamSynchronize(P->hstream[b]);
-    if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    if (e != cudaSuccess) return drain(cuda_fail(e, "stream synchronize"));
   }
   return QED_OK;
 }
@@ -403,6 +446,8 @@ qed_status qed_mc_sum(const qed_process* proc, const qed_mc_config* cfg, double*
   if (!(cfg->omega_min >= 0.0)) return fail(QED_ERR_INVALID_ARGUMENT, "omega_min must be >= 0");
   if (cfg->n_points == 0) return QED_OK;
   if ((uintptr_t)partials & 7) return fail(QED_ERR_INVALID_ARGUMENT, "partials must be 8-byte aligned");
+  qed_status dst = check_device(proc->device);
+  if (dst != QED_OK) return dst;
   qed::QedEvalArgs a = proc->args;
   a.mom = nullptr;
   a.out = nullptr;

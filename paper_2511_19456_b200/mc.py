@@ -64,9 +64,12 @@ def mc_cross_section(proc, sqrt_s: float, omega_min: float, seed: int, n_total: 
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    partials = torch.zeros(3 * n_chunks(n_total), dtype=torch.float64, device=dev)
-    first, count = shard_range(n_total, rank, world)
-    if count:
-        proc.mc_sum(partials, sqrt_s, omega_min, seed, first, count, stream=stream)
-    reduce_partials(partials, group)
-    return cross_section(partials, n_total, sqrt_s, proc.n)
+    st = stream or torch.cuda.current_stream(dev)
+    # zero-fill, kernel, all-reduce and the D2H read all run in order on ONE stream
+    with torch.cuda.stream(st):
+        partials = torch.zeros(3 * n_chunks(n_total), dtype=torch.float64, device=dev)
+        first, count = shard_range(n_total, rank, world)
+        if count:
+            proc.mc_sum(partials, sqrt_s, omega_min, seed, first, count, stream=st)
+        reduce_partials(partials, group)
+        return cross_section(partials, n_total, sqrt_s, proc.n)

@@ -39,10 +39,11 @@ class _McConfig(ctypes.Structure):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("algorithm", ctypes.c_int), ("variant", ctypes.c_int)]
+    _fields_ = [("algorithm", ctypes.c_int), ("variant", ctypes.c_int), ("kernel_family", ctypes.c_int)]
 
 
 ALGORITHMS = {"cdag": 0, "bg": 1, "berends-giele": 1}
+KERNEL_FAMILIES = {"default": 0, "lane-group": 1}
 
 
 class ProcessInfo(ctypes.Structure):
@@ -105,14 +106,23 @@ def _stream_ptr(stream) -> int | None:
     return stream.cuda_stream
 
 
-def _ptr(t, n_min: int, name: str) -> int:
+def _ptr(t, numel: int, name: str, device=None, shape=None) -> int:
+    """Pointer of a contiguous float64 tensor with exactly ``numel`` elements (and ``shape``, when
+    given), on ``device`` (a cuda device index) or on the host (device=None)."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch tensor")
     if t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError(f"{name} must be contiguous float64")
-    if t.numel() < n_min:
-        raise ValueError(f"{name} has {t.numel()} elements, need {n_min}")
+    if device is None:
+        if t.is_cuda:
+            raise ValueError(f"{name} must be a host tensor for this entry point")
+    elif not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{name} must be on cuda:{device} (the handle's device), got {t.device}")
+    if shape is not None and t.dim() > 1 and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, need {tuple(shape)}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, need exactly {numel}")
     return t.data_ptr()
 
 
@@ -123,7 +133,7 @@ class Process:
     launch variant (None = default / QED_VARIANT)."""
 
     def __init__(self, n: int, n_in_photons: int = 1, in_spins=None, out_spins=None, algorithm: str = "cdag",
-                 variant: int | None = None):
+                 variant: int | None = None, kernel_family: str = "default"):
         self.n = n
         self.n_in_photons = n_in_photons
         self.n_out_photons = n + 1 - n_in_photons
@@ -147,10 +157,15 @@ class Process:
         if algorithm not in ALGORITHMS:
             raise ValueError(f"algorithm must be one of {sorted(ALGORITHMS)}")
         self.algorithm = algorithm
-        opt = _Options(ALGORITHMS[algorithm], -1 if variant is None else int(variant))
+        if kernel_family not in KERNEL_FAMILIES:
+            raise ValueError(f"kernel_family must be one of {sorted(KERNEL_FAMILIES)}")
+        opt = _Options(ALGORITHMS[algorithm], -1 if variant is None else int(variant), KERNEL_FAMILIES[kernel_family])
         _check(_lib.qed_process_create_ex(ctypes.byref(self._in), ctypes.byref(self._out), n, ctypes.byref(opt),
                                           ctypes.byref(h)), "qed_process_create_ex")
         self._h = h
+        import torch
+        # the library binds the handle to the current device (include/qed.h "Device binding")
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
 
     def close(self):
         if getattr(self, "_h", None):
@@ -168,22 +183,28 @@ class Process:
         _check(_lib.qed_get_process_info(self._h, ctypes.byref(inf)), "qed_get_process_info")
         return inf.as_dict()
 
+    def _soa(self, momenta_soa, n_points, device):
+        # the kernels read row r at momenta + r * n_points: the tensor must hold exactly
+        # 4 * n_ext rows of n_points (a wider batch would be read with the wrong row stride)
+        return _ptr(momenta_soa, 4 * self.n_ext * n_points, "momenta", device, (4 * self.n_ext, n_points))
+
     def eval_msq(self, momenta_soa, out, n_points: int | None = None, stream=None) -> None:
         """momenta_soa: cuda float64 [(4*n_ext), n_points] contiguous; out: cuda float64 [n_points]."""
         n_points = out.numel() if n_points is None else n_points
-        _check(_lib.qed_eval_msq(self._h, _ptr(momenta_soa, 4 * self.n_ext * n_points, "momenta"), n_points,
-                                 _ptr(out, n_points, "out"), _stream_ptr(stream)), "qed_eval_msq")
+        _check(_lib.qed_eval_msq(self._h, self._soa(momenta_soa, n_points, self.device), n_points,
+                                 _ptr(out, n_points, "out", self.device), _stream_ptr(stream)), "qed_eval_msq")
 
     def eval_msq_configs(self, momenta_soa, out, n_points: int, stream=None) -> None:
         H = 1 << self.n_ext
-        _check(_lib.qed_eval_msq_configs(self._h, _ptr(momenta_soa, 4 * self.n_ext * n_points, "momenta"),
-                                         n_points, _ptr(out, n_points * H, "out"), _stream_ptr(stream)),
+        _check(_lib.qed_eval_msq_configs(self._h, self._soa(momenta_soa, n_points, self.device), n_points,
+                                         _ptr(out, n_points * H, "out", self.device), _stream_ptr(stream)),
                "qed_eval_msq_configs")
 
-    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int) -> None:
+    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int | None = None) -> None:
         """Host buffers (pinned recommended): momenta [(4*n_ext), n_points], out [n_points]."""
-        _check(_lib.qed_eval_msq_host(self._h, _ptr(momenta_soa_host, 4 * self.n_ext * n_points, "momenta"),
-                                      n_points, _ptr(out_host, n_points, "out")), "qed_eval_msq_host")
+        n_points = out_host.numel() if n_points is None else n_points
+        _check(_lib.qed_eval_msq_host(self._h, self._soa(momenta_soa_host, n_points, None), n_points,
+                                      _ptr(out_host, n_points, "out", None)), "qed_eval_msq_host")
 
     def mc_sum(self, partials, sqrt_s: float, omega_min: float, seed: int, first_index: int, n_points: int,
                stream=None) -> None:
@@ -191,5 +212,7 @@ class Process:
         (float64, 3 * n_chunks, zeroed by the caller)."""
         cfg = _McConfig(float(sqrt_s), float(omega_min), int(seed), int(first_index), int(n_points))
         n_chunks = (first_index + n_points + MC_CHUNK - 1) // MC_CHUNK
-        _check(_lib.qed_mc_sum(self._h, ctypes.byref(cfg), _ptr(partials, 3 * n_chunks, "partials"),
+        if partials.numel() < 3 * n_chunks:
+            raise ValueError(f"partials has {partials.numel()} elements, need >= {3 * n_chunks}")
+        _check(_lib.qed_mc_sum(self._h, ctypes.byref(cfg), _ptr(partials, partials.numel(), "partials", self.device),
                                _stream_ptr(stream)), "qed_mc_sum")

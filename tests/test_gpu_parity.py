@@ -83,39 +83,53 @@ def test_compton_lab_klein_nishina_config(qed):
             assert np.max(np.abs(got / ref - 1)) <= TOL
 
 
-@pytest.mark.parametrize("n", [2, 3])
-def test_fixed_states_match_oracle(qed, n):
-    mom = synthetic.rambo_cm(n, 301, seed=3000 + n)
+FIXED_POINTS = {1: 301, 2: 301, 3: 301, 4: 67, 5: 13}
+
+
+@pytest.mark.parametrize("algorithm", ["cdag", "bg"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_fixed_states_match_oracle(qed, n, algorithm):
+    """Random partial specs (each particle summed or fixed to 0/1), plus the all-fixed spec, in a
+    boosted frame where no momentum lies along z (so every state label matters)."""
+    mom = synthetic.boost_rotate(synthetic.rambo_cm(n, FIXED_POINTS[n], seed=3000 + n), seed=31)
     rng = np.random.default_rng(n)
-    for _ in range(3):
-        spec = [int(x) for x in rng.integers(-1, 2, size=n + 3)]
-        proc = qed.Process(n, in_spins=spec[:2], out_spins=spec[2:])
+    specs = [[int(x) for x in rng.integers(-1, 2, size=n + 3)] for _ in range(3)]
+    specs.append([int(x) for x in rng.integers(0, 2, size=n + 3)])
+    scale = oracle.msq(1, n, mom.numpy())
+    for spec in specs:
+        proc = qed.Process(n, in_spins=spec[:2], out_spins=spec[2:], algorithm=algorithm)
         got = _gpu_msq(qed, proc, mom)
         ref = oracle.msq(1, n, mom.numpy(), spec=spec)
-        scale = oracle.msq(1, n, mom.numpy())
-        assert np.max(np.abs(got - ref) / scale) <= TOL
+        assert np.max(np.abs(got - ref) / scale) <= TOL, spec
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4])
-def test_paper_direction_matches_oracle(qed, n):
+@pytest.mark.parametrize("algorithm", ["cdag", "bg"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_paper_direction_matches_oracle(qed, n, algorithm):
     """e- gamma^n -> e- gamma: n incoming photons.  Kinematics from
     RAMBO for the north-star process with the photon roles crossed is not physical, so
     build it directly: RAMBO 2 -> (e + gamma) final state from an initial e- + n gamma
     system generated as the 'final' state of a north-star point, reversed."""
-    mom = synthetic.rambo_cm(n, 257, sqrt_s=5.0, seed=4000 + n).numpy()
+    mom = synthetic.rambo_cm(n, {5: 37, 4: 131}.get(n, 257), sqrt_s=5.0, seed=4000 + n).numpy()
     # time-reverse the north-star kinematics: initial <-> final (momenta unchanged)
     # north-star order: e_in, g_in, e_out, g_out*n  ->  paper order: e_in', g_in'*n, e_out', g_out'
     rev = np.concatenate([mom[:, 2:3], mom[:, 3:], mom[:, 0:1], mom[:, 1:2]], axis=1)
-    proc = qed.Process(n, n_in_photons=n)
+    proc = qed.Process(n, n_in_photons=n, algorithm=algorithm)
     got = _gpu_msq(qed, proc, torch.from_numpy(rev))
     ref = oracle.msq(n, 1, rev)
     assert np.max(np.abs(got / ref - 1)) <= TOL
+    # fixed states in the paper direction (the paper evaluates one configuration per call, PAPER.md:159)
+    spec = [0] + [1, 0] * n
+    spec = spec[:n + 3]
+    proc = qed.Process(n, n_in_photons=n, in_spins=spec[:n + 1], out_spins=spec[n + 1:], algorithm=algorithm)
+    got = _gpu_msq(qed, proc, torch.from_numpy(rev))
+    assert np.max(np.abs(got - oracle.msq(n, 1, rev, spec=spec)) / ref) <= TOL
 
 
 def test_empty_and_single_point(qed):
     proc = qed.Process(2)
-    soa = torch.zeros((4 * 5, 1), dtype=torch.float64, device="cuda")
-    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    soa = torch.zeros((4 * 5, 0), dtype=torch.float64, device="cuda")
+    out = torch.zeros(0, dtype=torch.float64, device="cuda")
     proc.eval_msq(soa, out, n_points=0)
     torch.cuda.synchronize()
     mom = synthetic.rambo_cm(2, 1, seed=5)
@@ -132,7 +146,7 @@ def test_ragged_sizes_n2(qed, npts):
     assert np.max(np.abs(got / oracle.msq(1, 2, mom.numpy()) - 1)) <= TOL
 
 
-@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 2048), (3, 1 << 20, 512), (5, 1 << 16, 24)])
+@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 2048), (3, 1 << 21, 512), (4, 1 << 20, 64), (5, 1 << 18, 24)])
 def test_full_size_sampled(qed, n, npts, sample):
     """Bench-sized batches (the launch configuration bench.py times): sampled outputs vs the oracle."""
     torch.manual_seed(0)
@@ -161,6 +175,39 @@ def test_abi_errors(qed):
     assert st == 1
     st = qed.library().qed_eval_msq(proc._h, None, -1, None, None)
     assert st == 1
+    # the binding refuses layouts the kernels would misread (row stride = n_points)
+    soa = torch.zeros((4 * 4, 10), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        proc.eval_msq(soa, torch.zeros(5, dtype=torch.float64, device="cuda"))   # wider batch than out
+    with pytest.raises(ValueError):
+        proc.eval_msq(soa.cpu(), torch.zeros(10, dtype=torch.float64, device="cuda"))   # host momenta
+    with pytest.raises(ValueError):
+        proc.eval_msq_host(soa, torch.zeros(10, dtype=torch.float64), 10)                # device momenta
+    with pytest.raises(qed.QedError):
+        qed.Process(2, kernel_family="default", variant=10 ** 6)
+
+
+def test_env_variant_out_of_range_is_an_error(qed, monkeypatch):
+    """QED_VARIANT that is not a compiled variant index fails loudly (no silent fallback)."""
+    nv = qed.Process(3).info()["n_variants"]
+    for bad in (str(nv), "-3", "x"):
+        monkeypatch.setenv("QED_VARIANT", bad)
+        with pytest.raises(qed.QedError) as e:
+            qed.Process(3)
+        assert e.value.status == 1
+    monkeypatch.setenv("QED_VARIANT", str(nv - 1))
+    assert qed.Process(3).info()["variant"] == nv - 1
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_lane_group_family_at_small_n(qed, n):
+    """kernel_family="lane-group" runs the lane-group kernel at n <= 2 (same results)."""
+    mom = synthetic.rambo_cm(n, 1029, seed=3300 + n)
+    for algorithm in ("cdag", "bg"):
+        proc = qed.Process(n, algorithm=algorithm, kernel_family="lane-group")
+        assert proc.info()["lanes_per_point"] == 1 << (n + 1)
+        got = _gpu_msq(qed, proc, mom)
+        assert np.max(np.abs(got / oracle.msq(1, n, mom.numpy()) - 1)) <= TOL
 
 
 def test_host_entry_point(qed):
@@ -246,7 +293,8 @@ def test_bg_paper_direction_and_fixed_states(qed, n):
     assert np.max(np.abs(got - ref) / oracle.msq(1, n, mom)) <= TOL
 
 
-@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 1024), (5, 1 << 18, 24)])
+@pytest.mark.parametrize("n,npts,sample", [(2, 1 << 22, 1024), (3, 1 << 21, 512), (4, 1 << 20, 64),
+                                           (5, 1 << 18, 24), (6, 1 << 18, 4)])
 def test_bg_full_size_sampled(qed, n, npts, sample):
     mom = synthetic.rambo_cm(n, npts, sqrt_s=5.0, seed=7100 + n, device="cuda")
     out = torch.empty(npts, dtype=torch.float64, device="cuda")

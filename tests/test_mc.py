@@ -200,3 +200,27 @@ def test_gpu_mc_sum_bg_n6_matches_oracle():
     assert np.array_equal(got[:, 2], ref[:, 2])
     nz = ref[:, 0] > 0
     assert np.all(np.abs(got[nz, :2] / ref[nz, :2] - 1) <= 1e-10)
+
+
+@pytest.mark.gpu
+def test_gpu_mc_sum_full_size_sampled_chunks():
+    """BASELINE.json configs[3] at its stated size: n = 4, 2^24 points in one qed_mc_sum call (the
+    launch bench.py times), both algorithms; 8 sampled chunks of 1024 points (first, last, 6 random)
+    recomputed one by one by the oracle.  Cut counts bit-equal, sums within 1e-10."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_19456_b200 import qed
+    n, N, sqrt_s, om, seed = 4, 1 << 24, 5.0, 0.25, 4
+    nch = mc.n_chunks(N)
+    rng = np.random.default_rng(4)
+    chunks = sorted({0, nch - 1, *rng.integers(1, nch - 1, size=6).tolist()})
+    while len(chunks) < 8:
+        chunks = sorted(set(chunks) | {int(rng.integers(1, nch - 1))})
+    ref = np.stack([oracle.mc_sum(n, sqrt_s, om, seed, c * mc.CHUNK, mc.CHUNK)[c] for c in chunks])
+    for algorithm in ("bg", "cdag"):
+        partials = torch.zeros(3 * nch, dtype=torch.float64, device="cuda")
+        qed.Process(n, algorithm=algorithm).mc_sum(partials, sqrt_s, om, seed, 0, N)
+        torch.cuda.synchronize()
+        got = partials.cpu().numpy().reshape(nch, 3)[chunks]
+        assert np.array_equal(got[:, 2], ref[:, 2]), algorithm
+        assert np.all(np.abs(got[:, :2] / ref[:, :2] - 1) <= 1e-10), algorithm
