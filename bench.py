@@ -12,8 +12,12 @@ data-path collective), time = max over ranks of the CUDA-event time.
 
 Prints ONE JSON line (rank 0).  Extra keys: roofline (FP64 ALU bound, DESIGN.md
 "Roofline"), cpu_baseline (the oracle on a bounded sample), e2e (public host API
-with H2D/D2H inside the timed region), clocks, gpu_launches, per_n (the other
-process sizes at their own batch sizes, same timing protocol, fewer steps).
+with H2D/D2H inside the timed region), clocks (NVML polled every 2 ms inside the
+timed region), gpu_launches, per_n (the other process sizes at their BASELINE
+config sizes, same timing protocol, fewer steps), and one block per multi-GPU config
+of BASELINE.json: c3_strong (n = 3, 2^24 points in total split over the ranks),
+c4_mc (n = 4, 2^24 points, MC kernel and NCCL all-reduce timed separately) and
+c5_strong (n = 5, 2^26 points in total split over the ranks).
 """
 from __future__ import annotations
 
@@ -32,7 +36,10 @@ sys.path.insert(0, ROOT)
 METRIC = "|M|^2 evals/sec (phase-space pts/s) e-gamma->e-+n gamma"
 UNIT = "points/s"
 FP64_PEAK_TFLOPS = 148 * 128 * 1.965e9 / 1e12   # 148 SM x 64 DFMA/clk x 2 flop x 1965 MHz
-PER_N_POINTS = {1: 1 << 22, 2: 1 << 22, 3: 1 << 21, 4: 1 << 20, 5: 1 << 18, 6: 1 << 18, 7: 1 << 16, 8: 1 << 14}
+# per-GPU batch of each size: BASELINE.json configs (C2 n=2 2^22; C3 n=3 2^24; C4 n=4 2^24; C5 n=5 2^26 over
+# 8 GPUs = 2^23 per GPU); n = 1 (C1 is 4096 points, too small to time) and BG n = 6..8 sized to ~0.1-0.5 s
+PER_N_POINTS = {1: 1 << 22, 2: 1 << 22, 3: 1 << 24, 4: 1 << 24, 5: 1 << 23, 6: 1 << 20, 7: 1 << 18, 8: 1 << 16}
+GEN_CHUNK = 1 << 20     # points per generator call for the strong-scaling configs (seed keyed by chunk index)
 
 
 def parse():
@@ -52,6 +59,9 @@ def parse():
     ap.add_argument("--no-mc", action="store_true", help="skip the MC cross-section leg (configs[3])")
     ap.add_argument("--algorithm", default="cdag", choices=["cdag", "bg"],
                     help="cdag: the paper's node-reduced diagram DAG (headline); bg: Berends-Giele rewrite")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c3_strong / c4_mc / c5_strong blocks")
+    ap.add_argument("--config-shrink", type=int, default=0,
+                    help="divide the c3/c4/c5 totals by 2^k (plumbing tests only; the lines then say so)")
     return ap.parse_args()
 
 
@@ -97,6 +107,56 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
+class NvmlSampler:
+    """SM clock and clock-event reasons polled every `period` s from a thread (NVML), so that even a
+    30 ms timed region carries ~15 samples.  Device found by PCI bus id (NVML and CUDA indices can differ)."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, cuda_index: int, period: float = 0.002):
+        self.period = period
+        self.h = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(cuda_index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = None
+
+    def start(self):
+        import threading
+        self.samples, self.reasons, self.stop_flag = [], 0, False
+        if self.h is None:
+            return
+        self.max_mhz = self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+
+        def run():
+            while not self.stop_flag:
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    pass
+                time.sleep(self.period)
+        self.th = threading.Thread(target=run, daemon=True)
+        self.th.start()
+
+    def stop(self) -> dict:
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "source": "nvml"}
+        self.stop_flag = True
+        self.th.join()
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(sm),
+                "reasons": sorted(k for k, b in self.REASONS.items() if self.reasons & b),
+                "source": f"NVML polled every {self.period * 1e3:.0f} ms inside the timed region"}
+
+
 # ---------------------------------------------------------------- distributed plumbing
 DIST_BACKEND = os.environ.get("QED_BENCH_DIST_BACKEND", "nccl")   # "gloo": multi-rank plumbing test on one GPU
 def dist_setup(gpus: int):
@@ -106,6 +166,10 @@ def dist_setup(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # communicator set-up lines (ranks, NVLS / NVLink transport) on stderr: stdout carries the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if DIST_BACKEND == "gloo":
             # plumbing check on a box with fewer GPUs than ranks (tests only: ranks share devices,
             # so the timings are not scaling numbers)
@@ -248,39 +312,105 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- our arm
-def run_mc(args, world, rank, stream, dev) -> dict:
-    """BASELINE.json configs[3]: e- gamma -> e- + 4 gamma, 2^24 points in total, Monte-Carlo cross-section:
-    each rank generates + evaluates its chunk-aligned share on its GPU (fused qed_mc_sum), then ONE
-    all_reduce of the chunk partial sums (NCCL on the GPU box).  Timed with CUDA events around the whole
-    step (kernel + all-reduce), max over ranks.  Both algorithms give the same sigma (same points)."""
+def gen_soa_range(n: int, first_chunk: int, n_chunks_: int, chunk: int, sqrt_s: float, seed: int, dev):
+    """SoA momenta of global chunks [first_chunk, first_chunk + n_chunks_) of a point set that does not
+    depend on how it is split: chunk c comes from its own generator seeded (seed, c)."""
     import torch
 
+    import synthetic
+    soa = torch.empty((4 * (n + 3), n_chunks_ * chunk), dtype=torch.float64, device=dev)
+    for j in range(n_chunks_):
+        m = synthetic.rambo_cm(n, chunk, sqrt_s=sqrt_s, seed=seed * 1000003 + first_chunk + j, device=dev)
+        soa[:, j * chunk:(j + 1) * chunk] = synthetic.to_soa(m)
+        del m
+    return soa
+
+
+def run_strong(args, world, rank, stream, dev, n: int, total: int, seed: int, algorithms, steps: int,
+               warmup: int, label: str) -> dict:
+    """Strong scaling: `total` points in all, rank r evaluates its contiguous share of the global chunks;
+    time = max over ranks of the CUDA-event time of `steps` calls; value = total / (time per step)."""
+    import torch
+
+    from paper_2511_19456_b200 import qed
+    chunk = min(GEN_CHUNK, total >> 3)   # independent of the rank count: the point set is fixed
+    nch = total // chunk
+    c0, c1 = nch * rank // world, nch * (rank + 1) // world
+    soa = gen_soa_range(n, c0, c1 - c0, chunk, args.sqrt_s, seed, dev)
+    P = soa.shape[1]
+    out = torch.empty(max(P, 1), dtype=torch.float64, device=dev)
+    res = {"workload": label, "n": n, "points_total": total, "points_this_rank": P, "scaling": "strong",
+           "ranks": world, "steps": steps, "warmup": warmup}
+    for algo in algorithms:
+        proc = qed.Process(n, algorithm=algo)
+        fpp = proc.info()["flops_per_point"]
+        t, per = time_device(lambda: proc.eval_msq(soa, out[:P], P, stream=stream) if P else None, steps, warmup,
+                             world, stream)
+        per_rank_s = statistics.mean(per) / 1e3 if per else 0.0
+        res[algo] = {"value": total * steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps,
+                     "flops_per_point": fpp,
+                     "frac_fp64_peak_rank0": round(fpp * P / per_rank_s / 1e12 / FP64_PEAK_TFLOPS, 4) if P else None}
+        del proc
+    del soa, out
+    return res
+
+
+def run_mc(args, world, rank, stream, dev, shrink: int = 0) -> dict:
+    """BASELINE.json configs[3]: e- gamma -> e- + 4 gamma, 2^24 points in total, Monte-Carlo cross-section.
+    Each rank generates + evaluates its chunk-aligned share on its GPU (fused qed_mc_sum), then ONE
+    all_reduce of the zero-padded chunk partial sums (NCCL on the GPU box), then the fixed-order chunk
+    sum on the host.  The three phases are timed separately over 5 iterations (after 2 warm-up ones):
+    kernel and all-reduce with CUDA events on the launching stream (max over ranks), host sum with
+    perf_counter.  Both algorithms give the same sigma (same points, chunk-aligned shards)."""
+    import torch
+    import torch.distributed as dist
+
     from paper_2511_19456_b200 import mc, qed
-    out = {"n": 4, "points_total": 1 << 24, "sqrt_s": args.sqrt_s, "omega_min": 0.05 * args.sqrt_s}
+    N = (1 << 24) >> shrink
+    om = 0.05 * args.sqrt_s
+    out = {"workload": "BASELINE configs[3]: e-gamma->e-+4gamma MC cross-section, all-reduced", "n": 4,
+           "points_total": N, "sqrt_s": args.sqrt_s, "omega_min": om, "iterations": 5, "warmup": 2,
+           "scaling": "strong", "ranks": world, "sigma_unit": "m_e^-2 (natural units)",
+           "collective": "all_reduce(SUM) of 3 x n_chunks doubles" + (" (NCCL)" if world > 1 and DIST_BACKEND == "nccl"
+                                                                      else " (gloo)" if world > 1 else " (none, 1 rank)")}
+    first, count = mc.shard_range(N, rank, world)
+    nch = mc.n_chunks(N)
     for algo in ("bg", "cdag"):
         proc = qed.Process(4, algorithm=algo)
-        N = out["points_total"]
-        res = {}
-
-        def step():
-            res.update(mc.mc_cross_section(proc, args.sqrt_s, 0.05 * args.sqrt_s, 4, N, device=dev, stream=stream))
-        step()
-        torch.cuda.synchronize()
-        barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t = max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
-        out[algo] = {"value": N / t, "unit": UNIT, "ms": 1e3 * t, "sigma": res["sigma"], "error": res["error"],
-                     "n_pass": res["n_pass"]}
-    out["sigma_unit"] = "m_e^-2 (natural units)"
+        kern, red, host = [], [], []
+        res = None
+        for it in range(7):
+            with torch.cuda.stream(stream):
+                partials = torch.zeros(3 * nch, dtype=torch.float64, device=dev)
+                torch.cuda.synchronize()
+                barrier(world)
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(stream)
+                if count:
+                    proc.mc_sum(partials, args.sqrt_s, om, 4, first, count, stream=stream)
+                e[1].record(stream)
+                mc.reduce_partials(partials)
+                e[2].record(stream)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = mc.cross_section(partials, N, args.sqrt_s, 4)
+                th = time.perf_counter() - t0
+            if it >= 2:
+                kern.append(e[0].elapsed_time(e[1]) / 1e3)
+                red.append(e[1].elapsed_time(e[2]) / 1e3)
+                host.append(th)
+        k = max_over_ranks(world, statistics.mean(kern))
+        r = max_over_ranks(world, statistics.mean(red))
+        h = statistics.mean(host)
+        out[algo] = {"value": N / (k + r), "unit": UNIT, "kernel_ms": 1e3 * k, "allreduce_ms": 1e3 * r,
+                     "host_sum_ms": 1e3 * h, "value_incl_host_sum": N / (k + r + h),
+                     "sigma": res["sigma"], "error": res["error"], "n_pass": res["n_pass"]}
     return out
 
 
 def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool = False) -> dict:
-    """Every process size at its own batch size, same timing protocol, 5 steps.  paper_direction:
+    """Every process size at its BASELINE config batch size (PER_N_POINTS), same timing protocol: 3 warm-up
+    + 5 timed steps, or 1 + 2 when one step takes over 0.5 s (CDAG n = 5).  paper_direction:
     e- gamma^n -> e- gamma (time-reversed RAMBO kinematics), same kernels."""
     import torch
 
@@ -288,7 +418,7 @@ def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool 
     from paper_2511_19456_b200 import qed
     out = {}
     for m in range(1, 9 if algorithm == "bg" else 6):
-        Pm = PER_N_POINTS[m] * (4 if algorithm == "bg" and 4 <= m <= 5 else 1)
+        Pm = PER_N_POINTS[m]
         pm = qed.Process(m, n_in_photons=m if paper_direction else 1, algorithm=algorithm)
         mm = synthetic.rambo_cm(m, Pm, sqrt_s=args.sqrt_s, seed=7 + m, device=dev)
         if paper_direction:   # initial <-> final: e_in' = e_out, gamma_in' = gamma_out..., e_out' = e_in, gamma_out' = gamma_in
@@ -296,11 +426,13 @@ def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool 
         sm = synthetic.to_soa(mm)
         del mm
         om = torch.empty(Pm, dtype=torch.float64, device=dev)
-        tm, perm = time_device(lambda: pm.eval_msq(sm, om, Pm, stream=stream), 5, 3, world, stream)
+        t1, _ = time_device(lambda: pm.eval_msq(sm, om, Pm, stream=stream), 1, 1, world, stream)
+        K, W = (2, 0) if t1 > 0.5 else (5, 2)
+        tm, perm = time_device(lambda: pm.eval_msq(sm, om, Pm, stream=stream), K, W, world, stream)
         fm = pm.info()["flops_per_point"]
         ks = statistics.mean(perm) / 1e3
-        out[str(m)] = {"points_per_gpu": Pm, "value": world * Pm * 5 / tm, "unit": UNIT,
-                       "ms_per_step": 1e3 * tm / 5, "flops_per_point": fm,
+        out[str(m)] = {"points_per_gpu": Pm, "value": world * Pm * K / tm, "unit": UNIT, "steps": K,
+                       "ms_per_step": 1e3 * tm / K, "flops_per_point": fm,
                        "achieved_tflops": round(fm * Pm / ks / 1e12, 3),
                        "frac_fp64_peak": round(fm * Pm / ks / 1e12 / FP64_PEAK_TFLOPS, 4)}
         del sm, om, pm
@@ -340,7 +472,9 @@ def run_b200(args, world, rank, local):
     del mom
     out = torch.empty(P, dtype=torch.float64, device=dev)
     launches0 = qed.launch_count()
-    clocks = ClockSampler(local)
+    clocks = NvmlSampler(local)
+    smi = ClockSampler(local)
+    smi.start()
 
     def step():
         proc.eval_msq(soa, out, P, stream=stream)
@@ -349,7 +483,7 @@ def run_b200(args, world, rank, local):
         step()
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.02)
     total, per = time_device(step, args.steps, 0, world, stream)
     clk = clocks.stop()
     launches = qed.launch_count() - launches0 - args.warmup
@@ -379,13 +513,39 @@ def run_b200(args, world, rank, local):
         per_n_bg = sweep_per_n(args, world, stream, dev, "bg")
         per_n_paper = sweep_per_n(args, world, stream, dev, "cdag", paper_direction=True)
 
-    mc_res = None if args.no_mc else run_mc(args, world, rank, stream, dev)
+    mc_res = None if args.no_mc else run_mc(args, world, rank, stream, dev, args.config_shrink)
+    c3 = c5 = None
+    if not args.no_configs:
+        k = args.config_shrink
+        c3 = run_strong(args, world, rank, stream, dev, 3, (1 << 24) >> k, 3, ("cdag", "bg"), 5, 3,
+                        "BASELINE configs[2]: e-gamma->e-+3gamma, 2^24 points in total" + (f" >> {k}" if k else ""))
+        c5 = run_strong(args, world, rank, stream, dev, 5, (1 << 26) >> k, 5, ("bg", "cdag"), 2, 1,
+                        "BASELINE configs[4]: e-gamma->e-+5gamma, 2^26 points in total, all 256 configurations"
+                        + (f" >> {k}" if k else ""))
+    clk_smi = smi.stop()
 
+    peak = None
+    if rank == 0:
+        pk = NvmlSampler(local)
+        pk.start()
+        peak = measure_fp64_peak()
+        if peak is not None:
+            peak["clocks"] = pk.stop()
+            if peak["clocks"].get("sm_mhz"):
+                peak["frac_of_nominal_at_observed_clock"] = round(
+                    peak["tflops"] / (148 * 128 * peak["clocks"]["sm_mhz"] * 1e6 / 1e12), 4)
+        else:
+            pk.stop()
+    # every collective is done: the other ranks leave, so rank 0's oracle baseline has the host to itself
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = oracle_rate(n, 12.0, args.sqrt_s, args.seed)
         cpu["cpu"] = cpu_model()
-    peak = measure_fp64_peak() if rank == 0 else None
+        if world > 1:
+            cpu["note"] = f"rank 0 after the other {world - 1} ranks finished (host idle otherwise)"
 
     if rank == 0:
         line = {
@@ -399,10 +559,11 @@ def run_b200(args, world, rank, local):
                        "parallelism": f"points sharded over {world} GPU(s), no collective",
                        "l2": "inputs > 126 MB L2 (no flush needed)",
                        "kernel": dict({k: info[k] for k in ("lanes_per_point", "warps_per_block", "smem_per_block",
-                                                            "grid_blocks")}, variant=os.environ.get("QED_VARIANT", "0"))},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-            "fp64_dfma_microbench": peak, "per_n": per_n,
+                                                            "grid_blocks", "variant")})},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "clocks_whole_run": clk_smi,
+            "gpu_launches": launches, "fp64_dfma_microbench": peak, "per_n": per_n,
             "per_n_berends_giele": per_n_bg, "per_n_paper_direction": per_n_paper, "mc": mc_res,
+            "c3_strong": c3, "c5_strong": c5,
         }
         print(json.dumps(line), flush=True)
 

@@ -119,8 +119,7 @@ def test_paper_direction_matches_oracle(qed, n, algorithm):
     ref = oracle.msq(n, 1, rev)
     assert np.max(np.abs(got / ref - 1)) <= TOL
     # fixed states in the paper direction (the paper evaluates one configuration per call)
-    spec = [0] + [1, 0] * n
-    spec = spec[:n + 3]
+    spec = ([0] + [1, 0] * (n + 2))[:n + 3]
     proc = qed.Process(n, n_in_photons=n, in_spins=spec[:n + 1], out_spins=spec[n + 1:], algorithm=algorithm)
     got = _gpu_msq(qed, proc, torch.from_numpy(rev))
     assert np.max(np.abs(got - oracle.msq(n, 1, rev, spec=spec)) / ref) <= TOL
