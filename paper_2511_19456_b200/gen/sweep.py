@@ -145,22 +145,58 @@ def emit_state(g: CDAG, proc: Process, name: str) -> tuple[str, int]:
     return "\n".join(L) + "\n", flops
 
 
-def emit_sweep_file(proc: Process, states: list[tuple[int, CDAG]]) -> tuple[str, list[dict]]:
-    """CUDA source with one kernel per CDAG state + a timing entry point; and per-state metadata."""
+def emit_sweep_files(proc: Process, states: list[tuple[int, CDAG]], stem: str) -> tuple[dict[str, str], list[dict]]:
+    """One translation unit per CDAG state (kernel k_state<k> + getter) and one with the timing entry
+    point, so that the states compile in parallel; and per-state metadata.  Returns ({file: source}, meta)."""
     N, nin = proc.N, proc.n_in_ph
-    funcs, meta = [], []
+    files, meta = {}, []
+    pre = _prelude(proc, len(states))
     for k, (done, g) in enumerate(states):
         src, fl = emit_state(g, proc, f"state{k}")
-        funcs.append(src)
         meta.append({"state": k, "reductions": done, "nodes": len(g), "predicted_flops": fl})
-    kernels = "\n".join(
-        f"__global__ void __launch_bounds__(128) k_state{k}(const double* __restrict__ mom, long long n, double* out, double norm) {{\n"
-        f"  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;\n"
-        f"  if (i < n) out[i] = norm * state{k}(mom, n, i);\n}}\n" for k in range(len(states)))
-    table = ", ".join(f"(const void*)k_state{k}" for k in range(len(states)))
-    src = f"""// GENERATED by paper_2511_19456_b200/gen/sweep.py -- node-reduction sweep (PAPER.md Fig. 9 analogue).
+        files[f"{stem}_s{k}.cu"] = (pre + src + f"""
+__global__ void __launch_bounds__(128) k_state{k}(const double* __restrict__ mom, long long n, double* out, double norm) {{
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = norm * state{k}(mom, n, i);
+}}
+}}  // namespace qed
+
+extern "C" const void* sweep_kernel_{k}(void) {{ return (const void*)qed::k_state{k}; }}
+""")
+    decl = "".join(f'extern "C" const void* sweep_kernel_{k}(void);\n' for k in range(len(states)))
+    table = ", ".join(f"sweep_kernel_{k}()" for k in range(len(states)))
+    files[f"{stem}_main.cu"] = f"""// GENERATED by paper_2511_19456_b200/gen/sweep.py -- timing entry point of the node-reduction sweep.
+#include <cuda_runtime.h>
+{decl}
+extern "C" int sweep_num_states(void) {{ return {len(states)}; }}
+// run state k over n points (momenta SoA on the device), reps timed launches; returns ms per launch
+extern "C" int sweep_run(int k, const double* mom, long long n, double* out, double norm, int reps, float* ms) {{
+  const void* kern[] = {{ {table} }};
+  if (k < 0 || k >= {len(states)}) return 1;
+  const int threads = 128;
+  const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+  void* args[] = {{(void*)&mom, (void*)&n, (void*)&out, (void*)&norm}};
+  cudaLaunchKernel(kern[k], dim3(blocks), dim3(threads), args, 0, 0);   // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) cudaLaunchKernel(kern[k], dim3(blocks), dim3(threads), args, 0, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float t = 0; cudaEventElapsedTime(&t, e0, e1);
+  *ms = t / reps;
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}}
+"""
+    return files, meta
+
+
+def _prelude(proc: Process, n_states: int) -> str:
+    N, nin = proc.N, proc.n_in_ph
+    return f"""// GENERATED by paper_2511_19456_b200/gen/sweep.py -- node-reduction sweep (PAPER.md Fig. 9 analogue).
 // Process e- + {nin} gamma -> e- + {proc.n_out_ph} gamma, fixed spins/polarisations (all 0), one thread per
-// point, one statement per CDAG compute node; {len(states)} reduction states.
+// point, one statement per CDAG compute node; {n_states} reduction states, one per translation unit.
 #include <cuda_runtime.h>
 #include "../qed_device.cuh"
 
@@ -231,29 +267,4 @@ __device__ __forceinline__ c2 sweep_join(const double* mom, long long n, long lo
   }}
   return r;
 }}
-{"".join(funcs)}
-{kernels}
-}}  // namespace qed
-
-extern "C" int sweep_num_states(void) {{ return {len(states)}; }}
-// run state k over n points (momenta SoA on the device), reps timed launches; returns ms per launch
-extern "C" int sweep_run(int k, const double* mom, long long n, double* out, double norm, int reps, float* ms) {{
-  static const void* kern[] = {{ {table.replace("k_state", "qed::k_state")} }};
-  if (k < 0 || k >= {len(states)}) return 1;
-  const int threads = 128;
-  const unsigned blocks = (unsigned)((n + threads - 1) / threads);
-  void* args[] = {{(void*)&mom, (void*)&n, (void*)&out, (void*)&norm}};
-  cudaLaunchKernel(kern[k], dim3(blocks), dim3(threads), args, 0, 0);   // warm-up
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
-  cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) cudaLaunchKernel(kern[k], dim3(blocks), dim3(threads), args, 0, 0);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float t = 0; cudaEventElapsedTime(&t, e0, e1);
-  *ms = t / reps;
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
-  return cudaGetLastError() == cudaSuccess ? 0 : 2;
-}}
 """
-    return src, meta

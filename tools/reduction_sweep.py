@@ -1,6 +1,6 @@
 """NEXT #4: node-reduction sweep on B200 (Fig. 9 analogue, lines 190-201).
 
-  build (here, no GPU):  python tools/reduction_sweep.py build [n]
+  build (here, no GPU):  python tools/reduction_sweep.py build   (build() compiles the libraries; this adds SASS sizes)
   run (GPU box):         python tools/reduction_sweep.py run [n]   -> gpurun_out/reduction_sweep_n{n}.json
 
 Generates the fixed-spin CDAG of e- gamma^n -> e- gamma at several partial node-reduction states
@@ -20,25 +20,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 GEN = os.path.join(ROOT, "paper_2511_19456_b200", "csrc", "generated")
 LIB = os.path.join(ROOT, "paper_2511_19456_b200", "lib")
-CHECK = [0.0, 0.125, 0.25, 0.5, 0.75, 1.0]
 
 
 def build(n):
-    from paper_2511_19456_b200.gen.dag import paper_process
-    from paper_2511_19456_b200.gen.sweep import emit_sweep_file, reduction_states
-    proc = paper_process(n)
-    states = reduction_states(proc, CHECK, seed=1)
-    src, meta = emit_sweep_file(proc, states)
-    cu = os.path.join(GEN, f"qed_sweep_n{n}.cu")
-    open(cu, "w").write(src)
-    json.dump(meta, open(os.path.join(LIB, f"sweep_n{n}_meta.json"), "w"))
-    nvcc = "/usr/local/cuda/bin/nvcc"
-    arch = ["-gencode", "arch=compute_100a,code=sm_100a"]
-    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(ROOT, "paper_2511_19456_b200", "csrc")]
-    for tag, flags in (("cse", ["-O3"]), ("nocse", ["-O3", "-DSWEEP_NOCSE"])):
+    """Compile (paper_2511_19456_b200.build, which also emits the states; n = 4 only) and record the
+    SASS instruction count of every state's kernel in each build."""
+    assert n == 4, "the sweep libraries are built for the paper's n = 4 process"
+    from paper_2511_19456_b200 import build as b
+    b.build()
+    mpath = os.path.join(LIB, f"sweep_n{n}_meta.json")
+    meta = json.load(open(mpath))
+    for tag in ("cse", "nocse"):
         out = os.path.join(LIB, f"libqed_sweep_n{n}_{tag}.so")
-        cmd = [nvcc] + arch + flags + inc + ["-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-o", out, cu]
-        subprocess.run(cmd, check=True)
         sass = subprocess.run(["cuobjdump", "-sass", out], capture_output=True, text=True).stdout
         counts, cur = {}, None
         for line in sass.splitlines():
@@ -49,7 +42,7 @@ def build(n):
                 counts[cur] += 1
         for m in meta:
             m[f"sass_{tag}"] = next((v for k_, v in counts.items() if f"k_state{m['state']}E" in k_), None)
-    json.dump(meta, open(os.path.join(LIB, f"sweep_n{n}_meta.json"), "w"), indent=1)
+    json.dump(meta, open(mpath, "w"), indent=1)
     print(json.dumps(meta, indent=1))
 
 
