@@ -23,17 +23,20 @@ _LIBS = {
     "f80": os.path.join(_HERE, "liboracle_f80.so"),
 }
 _DEFS = {"f64": "double", "f80": "long double"}
+_ABC_SRC = os.path.join(_HERE, "abc_oracle.c")
+_ABC_LIB = os.path.join(_HERE, "liboracle_abc.so")
 _loaded: dict[str, ctypes.CDLL] = {}
 
 
 def build(force: bool = False) -> None:
-    """Compile the oracle (double and long-double builds) with gcc."""
-    for kind, path in _LIBS.items():
-        if not force and os.path.exists(path) and os.path.getmtime(path) >= os.path.getmtime(_SRC):
+    """Compile the oracles (QED in double and long double, ABC model in double) with gcc."""
+    jobs = [(path, _SRC, [f"-DORACLE_REAL={_DEFS[kind]}"]) for kind, path in _LIBS.items()]
+    jobs.append((_ABC_LIB, _ABC_SRC, []))
+    for path, src, defs in jobs:
+        if not force and os.path.exists(path) and os.path.getmtime(path) >= os.path.getmtime(src):
             continue
         tmp = path + f".tmp{os.getpid()}"
-        cmd = ["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", f"-DORACLE_REAL={_DEFS[kind]}",
-               "-o", tmp, _SRC, "-lm", "-lpthread"]
+        cmd = ["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC"] + defs + ["-o", tmp, src, "-lm", "-lpthread"]
         subprocess.run(cmd, check=True)
         os.replace(tmp, path)
 
@@ -187,3 +190,44 @@ def mc_sum(n_out_ph: int, sqrt_s: float, omega_min: float, seed: int, first: int
     if rc != 0:
         raise ValueError("oracle_mc_sum: bad arguments")
     return out.reshape(n_chunks, 3)
+
+
+# ---------------------------------------------------------------- ABC model (abc_oracle.c)
+
+def _abc():
+    if "abc" not in _loaded:
+        build()
+        lib = ctypes.CDLL(_ABC_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        lib.oracle_abc_msq.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                       dp, ctypes.c_long, dp, ctypes.c_int]
+        lib.oracle_abc_msq.restype = ctypes.c_int
+        lib.oracle_abc_diagram_sum.argtypes = [ctypes.c_int, dp, dp, ctypes.c_double, ctypes.c_double, dp]
+        lib.oracle_abc_diagram_sum.restype = ctypes.c_long
+        _loaded["abc"] = lib
+    return _loaded["abc"]
+
+
+def abc_msq(n_in: int, n_out: int, mom: np.ndarray, m_a: float, m_c: float, g: float = 1.0,
+            threads: int | None = None) -> np.ndarray:
+    """|M|^2 per point of A + n_in B -> A + n_out B.  mom: [n_points, n_in + n_out + 2, 4], particle
+    order A_in, B_in..., A_out, B_out...; the B mass enters only through the (on-shell) momenta."""
+    mom = np.ascontiguousarray(mom, dtype=np.float64)
+    assert mom.ndim == 3 and mom.shape[1:] == (n_in + n_out + 2, 4), mom.shape
+    out = np.empty(mom.shape[0], dtype=np.float64)
+    rc = _abc().oracle_abc_msq(n_in, n_out, m_a, m_c, g, _dp(mom), mom.shape[0], _dp(out),
+                               threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_abc_msq: bad arguments (the number of B-ons must be even)")
+    return out
+
+
+def abc_diagram_sum(q: np.ndarray, p_a: np.ndarray, m_a: float, m_c: float):
+    """(sum over orderings of prod 1/(Q_l^2 - m_{X_l}^2), number of diagrams) for signed B momenta q [N, 4]."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    p_a = np.ascontiguousarray(p_a, dtype=np.float64)
+    out = np.empty(1)
+    nd = _abc().oracle_abc_diagram_sum(q.shape[0], _dp(q), _dp(p_a), m_a, m_c, _dp(out))
+    if nd < 0:
+        raise ValueError("bad N")
+    return float(out[0]), int(nd)

@@ -104,6 +104,29 @@ def rambo_cm(n_out_photons: int, n_points: int, sqrt_s: float = 5.0, seed: int =
     return mom
 
 
+# ABC model (PAPER.md App. F): masses of the A-, B- and C-on in units of m_A (DESIGN.md reading A2)
+ABC_MASSES = (1.0, 0.5, 1.2)
+
+
+def abc_cm(n_out_b: int, n_points: int, sqrt_s: float = 5.0, seed: int = 2, masses=ABC_MASSES,
+           device="cpu") -> torch.Tensor:
+    """[n_points, n+3, 4] for A B -> A + n B in the CM frame at sqrt_s (incoming B along +z, A along -z),
+    final state from massive RAMBO with masses (m_A, m_B x n)."""
+    dev = torch.device(device)
+    g = _gen(seed, dev)
+    f64 = torch.float64
+    mA, mB, _ = masses
+    s = sqrt_s * sqrt_s
+    kin = math.sqrt((s - (mA + mB) ** 2) * (s - (mA - mB) ** 2)) / (2 * sqrt_s)
+    n = n_out_b
+    mom = torch.empty((n_points, n + 3, 4), dtype=f64, device=dev)
+    mom[:, 0] = torch.tensor([math.sqrt(mA * mA + kin * kin), 0.0, 0.0, -kin], dtype=f64, device=dev)
+    mom[:, 1] = torch.tensor([math.sqrt(mB * mB + kin * kin), 0.0, 0.0, kin], dtype=f64, device=dev)
+    fin = _rambo_massive(n + 1, [mA] + [mB] * n, sqrt_s, n_points, g, dev)
+    mom[:, 2:] = fin.permute(1, 0, 2)
+    return mom
+
+
 def to_soa(mom: torch.Tensor) -> torch.Tensor:
     """[n_points, n_ext, 4] -> contiguous SoA [n_ext*4, n_points] (mom[(4j+mu)*n + i])."""
     n = mom.shape[0]
