@@ -439,6 +439,58 @@ def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool 
     return out
 
 
+def run_abc(args, world, stream, dev, qed_per_n) -> dict:
+    """ABC model (App. F, NEXT #3): A B -> A + n B at n = 1, 3, 5, 2^24 points per GPU, both
+    algorithms, same protocol as per_n; roofline per line (HBM when flops/byte is below the FP64 ridge,
+    FP64 ALU above it) and the kernel-weight ratio to QED e- gamma -> e- + n gamma of the same n
+    (same diagram structure, scalar instead of 4x4 kernels)."""
+    import torch
+
+    import synthetic
+    from paper_2511_19456_b200 import qed
+    hbm = hbm_peak_gbs()
+    ridge = FP64_PEAK_TFLOPS * 1e12 / (hbm * 1e9)
+    out = {"workload": "A B -> A + n B, RAMBO sqrt(s)=5 m_A, masses (m_A, m_B, m_C) = (1, 0.5, 1.2)",
+           "points_per_gpu": 1 << 24, "hbm_peak_gbs": hbm, "ridge_flop_per_byte": round(ridge, 2)}
+    P = 1 << 24
+    for n in (1, 3, 5):
+        mom = synthetic.abc_cm(n, P, sqrt_s=args.sqrt_s, seed=70 + n, device=dev)
+        soa = synthetic.to_soa(mom)
+        del mom
+        o = torch.empty(P, dtype=torch.float64, device=dev)
+        row = {}
+        for algo in ("cdag", "bg"):
+            proc = qed.AbcProcess(n, algorithm=algo)
+            inf = proc.info()
+            t, per = time_device(lambda: proc.eval_msq(soa, o, P, stream=stream), 10, 3, world, stream)
+            ks = statistics.mean(per) / 1e3
+            fl, by = inf["flops_per_point"], inf["bytes_per_point"]
+            if fl / by < ridge:
+                roof = {"bound": "hbm", "achieved": round(by * P / ks / 1e9, 1), "peak": hbm, "unit": "GB/s"}
+            else:
+                roof = {"bound": "alu", "achieved": round(fl * P / ks / 1e12, 3), "peak": round(FP64_PEAK_TFLOPS, 2),
+                        "unit": "TFLOP/s"}
+            roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+            row[algo] = {"value": world * P * 10 / t, "unit": UNIT, "ms_per_step": 1e3 * t / 10,
+                         "flops_per_point": fl, "bytes_per_point": by, "roofline": roof}
+            q = (qed_per_n or {}).get(str(n)) if algo == "cdag" else None
+            if q:
+                row[algo]["qed_same_n_points_per_s"] = q["value"]
+                row[algo]["abc_over_qed"] = round(row[algo]["value"] / q["value"], 1)
+            del proc
+        out[str(n)] = row
+        del soa, o
+    return out
+
+
+def hbm_peak_gbs() -> float:
+    """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def run_e2e(args, world, proc, soa, P) -> dict:
     """Same metric through the public host-buffer API (qed_eval_msq_host): every step copies the
     step's momenta H2D from pinned memory, evaluates, and copies |M|^2 back D2H."""
@@ -513,6 +565,7 @@ def run_b200(args, world, rank, local):
         per_n_bg = sweep_per_n(args, world, stream, dev, "bg")
         per_n_paper = sweep_per_n(args, world, stream, dev, "cdag", paper_direction=True)
 
+    abc = None if args.no_per_n else run_abc(args, world, stream, dev, per_n)
     mc_res = None if args.no_mc else run_mc(args, world, rank, stream, dev, args.config_shrink)
     c3 = c5 = None
     if not args.no_configs:
@@ -563,7 +616,7 @@ def run_b200(args, world, rank, local):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "clocks_whole_run": clk_smi,
             "gpu_launches": launches, "fp64_dfma_microbench": peak, "per_n": per_n,
             "per_n_berends_giele": per_n_bg, "per_n_paper_direction": per_n_paper, "mc": mc_res,
-            "c3_strong": c3, "c5_strong": c5,
+            "c3_strong": c3, "c5_strong": c5, "abc_model": abc,
         }
         print(json.dumps(line), flush=True)
 

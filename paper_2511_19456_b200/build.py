@@ -36,7 +36,7 @@ def nvcc() -> str:
 
 def _headers() -> list[str]:
     return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
-        [os.path.join(ROOT, "include", "qed.h")]
+        [os.path.join(ROOT, "include", "qed.h"), os.path.join(ROOT, "include", "abc.h")]
 
 
 def _compile(src: str, force: bool, extra=(), tag: str = "", log: bool = True) -> str:
@@ -93,14 +93,15 @@ def sweep_sources() -> tuple[list[str], str]:
 
 def build(force: bool = False, jobs: int | None = None) -> str:
     sys.path.insert(0, ROOT) if ROOT not in sys.path else None
+    from paper_2511_19456_b200.gen.abc import generate_abc
     from paper_2511_19456_b200.gen.emit import generate_all
     from paper_2511_19456_b200.gen.emit_bg import generate_bg
     from paper_2511_19456_b200.gen.emit_regs import generate_regs
 
     os.makedirs(OBJ_DIR, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
-    sources = generate_all(GEN_DIR) + generate_regs(GEN_DIR) + generate_bg(GEN_DIR) + \
-        [os.path.join(CSRC, "qed_runtime.cu")]
+    sources = generate_all(GEN_DIR) + generate_regs(GEN_DIR) + generate_bg(GEN_DIR) + generate_abc(GEN_DIR) + \
+        [os.path.join(CSRC, "qed_runtime.cu"), os.path.join(CSRC, "abc_runtime.cu")]
     sweep_src, _ = sweep_sources()
     units = [(s, (), "", True) for s in sources] + \
         [(s, fl, "_" + tag, False) for tag, fl in SWEEP_BUILDS.items() for s in sweep_src]

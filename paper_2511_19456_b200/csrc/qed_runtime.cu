@@ -164,6 +164,10 @@ struct qed_process {
 
 extern "C" {
 
+// shared with abc_runtime.cu (same library, same error slot and launch counter)
+qed_status qed_internal_fail(qed_status st, const char* msg) { return fail(st, msg); }
+void qed_internal_count_launch(void) { g_launches.fetch_add(1); }
+
 const char* qed_last_error(void) { return g_last_error.c_str(); }
 
 int64_t qed_launch_count(void) { return g_launches.load(); }

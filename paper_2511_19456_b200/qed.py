@@ -21,6 +21,7 @@ _STATUS = {0: "QED_OK", 1: "QED_ERR_INVALID_ARGUMENT", 2: "QED_ERR_UNSUPPORTED",
 
 EXPORTED = ["qed_process_create", "qed_process_create_ex", "qed_process_destroy", "qed_eval_msq", "qed_eval_msq_configs",
             "qed_eval_msq_host", "qed_mc_sum", "qed_get_process_info", "qed_last_error", "qed_launch_count"]
+EXPORTED_ABC = ["abc_process_create", "abc_process_destroy", "abc_eval_msq", "abc_get_process_info"]
 
 
 class QedError(RuntimeError):
@@ -57,6 +58,15 @@ class ProcessInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class AbcProcessInfo(ctypes.Structure):
+    _fields_ = [("n_b", ctypes.c_int), ("n_diagrams", ctypes.c_int), ("algorithm", ctypes.c_int),
+                ("grid_blocks", ctypes.c_int), ("threads_per_block", ctypes.c_int),
+                ("flops_per_point", ctypes.c_int64), ("bytes_per_point", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libqed.so not built ({LIB_PATH}); run `python -m paper_2511_19456_b200.build` "
@@ -73,6 +83,12 @@ def _load() -> ctypes.CDLL:
     lib.qed_eval_msq_host.argtypes = [vp, vp, i64, vp]
     lib.qed_mc_sum.argtypes = [vp, ctypes.POINTER(_McConfig), vp, vp]
     lib.qed_get_process_info.argtypes = [vp, ctypes.POINTER(ProcessInfo)]
+    lib.abc_process_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.abc_process_destroy.argtypes = [vp]
+    lib.abc_eval_msq.argtypes = [vp, vp, i64, vp, vp]
+    lib.abc_get_process_info.argtypes = [vp, ctypes.POINTER(AbcProcessInfo)]
+    for f in ("abc_process_create", "abc_process_destroy", "abc_eval_msq", "abc_get_process_info"):
+        getattr(lib, f).restype = ctypes.c_int
     lib.qed_last_error.restype = ctypes.c_char_p
     lib.qed_launch_count.restype = ctypes.c_int64
     for f in EXPORTED:
@@ -216,3 +232,46 @@ class Process:
             raise ValueError(f"partials has {partials.numel()} elements, need >= {3 * n_chunks}")
         _check(_lib.qed_mc_sum(self._h, ctypes.byref(cfg), _ptr(partials, partials.numel(), "partials", self.device),
                                _stream_ptr(stream)), "qed_mc_sum")
+
+
+# ABC model (include/abc.h): masses and coupling of the library (reading A2)
+ABC_MASS_A, ABC_MASS_B, ABC_MASS_C, ABC_COUPLING = 1.0, 0.5, 1.2, 1.0
+
+
+class AbcProcess:
+    """abc_process handle: A + n_in B -> A + n_out B (n_in + n_out even), algorithm "cdag" or "bg"."""
+
+    def __init__(self, n_out: int, n_in: int = 1, algorithm: str = "cdag"):
+        if algorithm not in ALGORITHMS:
+            raise ValueError(f"algorithm must be one of {sorted(ALGORITHMS)}")
+        self.n_in, self.n_out = n_in, n_out
+        self.n_ext = n_in + n_out + 2
+        self.algorithm = algorithm
+        h = ctypes.c_void_p()
+        _check(_lib.abc_process_create(n_in, n_out, ALGORITHMS[algorithm], ctypes.byref(h)), "abc_process_create")
+        self._h = h
+        import torch
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.abc_process_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        inf = AbcProcessInfo()
+        _check(_lib.abc_get_process_info(self._h, ctypes.byref(inf)), "abc_get_process_info")
+        return inf.as_dict()
+
+    def eval_msq(self, momenta_soa, out, n_points: int | None = None, stream=None) -> None:
+        """momenta_soa: cuda float64 [(4*n_ext), n_points]; out: cuda float64 [n_points]."""
+        n_points = out.numel() if n_points is None else n_points
+        mp = _ptr(momenta_soa, 4 * self.n_ext * n_points, "momenta", self.device, (4 * self.n_ext, n_points))
+        _check(_lib.abc_eval_msq(self._h, mp, n_points, _ptr(out, n_points, "out", self.device), _stream_ptr(stream)),
+               "abc_eval_msq")

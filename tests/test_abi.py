@@ -7,10 +7,10 @@ import re
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "qed.h")).read()
+def _declared_functions(header="qed.h", prefix="qed"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(qed_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(rf"\b({prefix}_[a-z_]+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_entry_points():
@@ -25,6 +25,24 @@ def test_library_exports_every_declared_symbol():
     missing = [f for f in _declared_functions() if not hasattr(lib, f)]
     assert not missing, missing
     assert set(qed.EXPORTED) <= set(_declared_functions())
+
+
+def test_library_exports_every_abc_symbol():
+    """include/abc.h (ABC model, App. F) is served by the same library."""
+    from paper_2511_19456_b200 import qed
+    names = _declared_functions("abc.h", "abc")
+    assert {"abc_process_create", "abc_eval_msq", "abc_process_destroy", "abc_get_process_info"} <= set(names)
+    missing = [f for f in names if not hasattr(qed.library(), f)]
+    assert not missing, missing
+
+
+def test_every_header_symbol_is_exported():
+    import glob
+    from paper_2511_19456_b200 import qed
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        for f in set(re.findall(r"^\s*(?:qed_status|const char\*|int64_t)\s+([a-z_]+)\s*\(", src, flags=re.M)):
+            assert hasattr(qed.library(), f), (h, f)
 
 
 def test_library_is_sm100a_only():
