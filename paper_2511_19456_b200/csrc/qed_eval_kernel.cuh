@@ -158,6 +158,77 @@ struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
   }
 };
 
+// ---- grouped Berends-Giele tasks (round 3; gen/lower_bg.py gtask): one descriptor computes the 2^F nodes
+// (S, spin, lam_fixed, mu) of one photon set S, mu = the polarisations of the LAST F photons of S (helicity
+// bits K-F+1..K).  Descriptor [mask, out_0, (parent_0, eps_0) per photon p of S, (leaf tasks:) h0] for node
+// mu = 0.  Interior levels are stored helicity-major, so node mu's output and parents sit at fixed strides
+// (doubles, gen/lower_bg.py group_strides): output SO mu; parent through a fixed photon SF mu; through a free
+// photon q SR (mu without bit q) -- loaded once for both of its polarisations (eps(lam = 1) 4 doubles after
+// eps(lam = 0), transverse: eps^3 = 0).  Leaf outputs: column swz(h0 + mu 2^(K-F+1)) of the rows at out_0.
+template <class T, int K, int F, int KIND, int SO, int SF, int SR>
+struct BGGroupFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
+  __device__ __forceinline__ void operator()(double* b, const Desc<T::DW>& raw) const {
+    if constexpr (F == 0) {
+      BGFn<T, K, KIND>{}(b, raw);
+    } else {
+      static_assert(F <= K, "free photons are photons of the node set");
+      constexpr bool ROW = KIND & 1;
+      constexpr int M = 1 << F, FX = K - F;
+      const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
+      spinor acc[M];
+#pragma unroll
+      for (int q = 0; q < F; ++q) {   // free photons first: their first vertex initialises every node
+        const int p = FX + q;
+        double e0[3], e1[2];
+        ld_eps(b + d[3 + 2 * p], e0);
+        const double2 t = *reinterpret_cast<const double2*>(b + d[3 + 2 * p] + 4);
+        e1[0] = t.x;
+        e1[1] = t.y;
+#pragma unroll
+        for (int mr = 0; mr < M / 2; ++mr) {
+          const spinor P = ld_aos<T::SP>(b, d[2 + 2 * p] + mr * SR);
+          const int mu0 = (mr & ((1 << q) - 1)) | ((mr >> q) << (q + 1)), mu1 = mu0 | (1 << q);
+          if (q == 0) {
+            acc[mu0] = ROW ? eslash_row(e0, P) : eslash_col(e0, P);
+            acc[mu1] = ROW ? eslash_row_t(e1, P) : eslash_col_t(e1, P);
+          } else {
+            if (ROW) { eslash_row_acc(e0, P, acc[mu0]); eslash_row_t_acc(e1, P, acc[mu1]); }
+            else { eslash_col_acc(e0, P, acc[mu0]); eslash_col_t_acc(e1, P, acc[mu1]); }
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < FX; ++p) {
+        double e[3];
+        ld_eps(b + d[3 + 2 * p], e);
+#pragma unroll
+        for (int mu = 0; mu < M; ++mu) {
+          const spinor P = ld_aos<T::SP>(b, d[2 + 2 * p] + mu * SF);
+          if (ROW) eslash_row_acc(e, P, acc[mu]);
+          else eslash_col_acc(e, P, acc[mu]);
+        }
+      }
+      if constexpr (KIND != 3) {
+        double m[5];
+        ld_mask(b + d[0], m);
+#pragma unroll
+        for (int mu = 0; mu < M; ++mu) acc[mu] = ROW ? prop_row(m, acc[mu]) : prop_col(m, acc[mu]);
+      }
+      if constexpr (KIND >= 2) {
+        const int h0 = d[2 + 2 * K];
+#pragma unroll
+        for (int mu = 0; mu < M; ++mu) {
+          const int h = h0 + (mu << (FX + 1));
+          st_leaf<KIND == 2 ? T::NHI : T::NHO>(b + d[1] + 2 * swz(h), acc[mu]);
+        }
+      } else {
+#pragma unroll
+        for (int mu = 0; mu < M; ++mu) st_aos<T::SP>(b, d[1] + mu * SO, acc[mu]);
+      }
+    }
+  }
+};
+
 // run_tasks8 split in two (BG T::SD / load_set / run_set_d): descriptors into registers ...
 template <class T, int COUNT, int OFF>
 __device__ __forceinline__ void load_tasks8(Desc<T::DW> (&d)[(COUNT + T::G - 1) / T::G], int g, const Desc<T::DW>* __restrict__ tbl) {

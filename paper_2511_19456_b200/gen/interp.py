@@ -162,6 +162,27 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     return out
 
 
+def expand_group(d, K: int, F: int, sp: int, leaf: bool, N: int) -> list[list[int]]:
+    """The 2^F single-node descriptors [mask, out, (parent, eps) x K] of grouped task d, by the kernel's
+    offset rules (qed_eval_kernel.cuh BGGroupFn; free photons = the last F of the node set)."""
+    from .lower_bg import group_strides, leaf_mu
+    if F == 0:
+        return [list(d[:2 + 2 * K])]
+    so, sf, sr = group_strides(K, F, math.comb(N, K), math.comb(N, K - 1) if K > 1 else 0)
+    res = []
+    for mu in range(1 << F):
+        e = [d[0], leaf_mu(d[1], d[2 + 2 * K], mu, K, F) if leaf else d[1] + so * sp * mu]
+        for p in range(K):
+            if p >= K - F:
+                q = p - (K - F)
+                mr = (mu & ((1 << q) - 1)) | ((mu >> (q + 1)) << q)
+                e += [d[2 + 2 * p] + sr * sp * mr, d[3 + 2 * p] + 4 * ((mu >> q) & 1)]
+            else:
+                e += [d[2 + 2 * p] + sf * sp * mu, d[3 + 2 * p]]
+        res.append(e)
+    return res
+
+
 def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     """Berends-Giele plan (gen/lower_bg.py) executed with the device layout; returns amplitudes
     in external bit order with e^N (same contract as eval_point)."""
@@ -225,8 +246,13 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
             acc = acc + f(sm[e: e + 3], get_aos(par))
         return acc
 
-    for kind, K, tasks in plan.levels:
-        for d in tasks:
+    SPP = plan.sp
+
+    def nodes(tasks, K, F, leaf=False):
+        return [e for d in tasks for e in expand_group(d, K, F, SPP, leaf, N)]
+
+    for kind, K, tasks, F in plan.levels:
+        for d in nodes(tasks, K, F):
             if kind == "in":
                 put_aos(d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
             else:
@@ -238,16 +264,16 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         if lb == 0:
             for sj in range(si, si + plan.setb):
                 for stage in plan.set_stages[sj]:
-                    for kind, K, tasks in stage:
-                        for d in tasks:
+                    for kind, K, tasks, F in stage:
+                        for d in nodes(tasks, K, F):
                             if kind == "in":
                                 put_aos(d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
                             else:
                                 put_aos(d[1], _prop_row(sm[d[0]: d[0] + 5], vsum(d, True)))
             for sj in range(si, si + plan.setb):
-                for d in plan.set_in[sj]:
+                for d in nodes(plan.set_in[sj], plan.j, plan.f_in, True):
                     put_leaf(plan.n_hi, d[1], _prop_col(sm[d[0]: d[0] + 5], vsum(d, False)))
-                for d in plan.set_out[sj]:
+                for d in nodes(plan.set_out[sj], N - plan.j, plan.f_out, True):
                     put_leaf(plan.n_ho, d[1], vsum(d, True))
         if si >= plan.n_sets_real:      # padding subset of a ragged last batch
             continue

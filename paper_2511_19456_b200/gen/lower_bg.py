@@ -30,6 +30,7 @@ from .lower import FLOPS, PITCH_BG, lane_offset, leaf_off
 
 FLOPS_BG = dict(FLOPS)
 FLOPS_BG["VACC"] = 48    # accumulating vertex: 8 real outputs x 3 fma
+FLOPS_BG["VACC_T"] = 32  # accumulating transverse vertex (eps^3 = 0, lam = 1 known at build time): 8 x 2 fma
 
 
 @dataclass
@@ -49,6 +50,9 @@ class BGPlan:
     flops: dict[str, int] = field(default_factory=dict)
     n_sets_real: int = 0     # C(N, j); sets[n_sets_real:] pad the last batch to SETB subsets
     hs: int = 1              # join halves (lower.hs_table): 1 = lane tile (s, s'); 2 = (s, s', lam_{N-1})
+    # node groups (round 3): F free polarisation bits per task of each stage kind; a task computes the 2^F
+    # nodes (S, spin, lam_fixed, mu) of one subset S, mu = the polarisations of the first F photons of S
+    grp: tuple = (0, 0, 0, 0, 0)   # (level 1, levels >= 2, in-leaf, out-leaf, recomputed levels)
 
     @property
     def H(self) -> int:
@@ -80,8 +84,8 @@ def lane_utilisation(plan) -> tuple[float, dict]:
     F = FLOPS_BG
     G, B, N = plan.G, plan.setb, plan.N
 
-    def cost(kind, K, leaf=False):
-        return F["V"] + (K - 1) * F["VACC"] + (F["S"] if (kind == "in" or not leaf) else 0)
+    def cost(kind, K, F=0, leaf=False):
+        return task_flops(K, F, kind == "in" or not leaf)
 
     def phase(groups):
         lane = [0.0] * G
@@ -93,24 +97,24 @@ def lane_utilisation(plan) -> tuple[float, dict]:
     phases = []
     i = 0
     while i < len(plan.levels):
-        kind, K, t = plan.levels[i]
-        grp = [(len(t), cost(kind, K), 0)]
+        kind, K, t, F0 = plan.levels[i]
+        grp = [(len(t), cost(kind, K, F0), 0)]
         if i + 1 < len(plan.levels) and plan.levels[i + 1][1] == K:
-            k2, _, t2 = plan.levels[i + 1]
-            grp.append((len(t2), cost(k2, K), lane_offset(len(t), G)))
+            k2, _, t2, F2 = plan.levels[i + 1]
+            grp.append((len(t2), cost(k2, K, F2), lane_offset(len(t), G)))
             i += 1
         phases.append(("int", phase(grp)))
         i += 1
     for _ in range(len(plan.sets) // B):
         for st in plan.set_stages[0]:
             grp, prev = [], 0
-            for q, (kind, K, t) in enumerate(st):
-                grp.append((len(t) * B, cost(kind, K), lane_offset(prev, G) if q > 0 else 0))
+            for q, (kind, K, t, F0) in enumerate(st):
+                grp.append((len(t) * B, cost(kind, K, F0), lane_offset(prev, G) if q > 0 else 0))
                 prev = len(t) * B
             phases.append(("rec", phase(grp)))
         n_in, n_out = B * len(plan.set_in[0]), B * len(plan.set_out[0])
-        phases.append(("leaf", phase([(n_in, cost("in", plan.j, True), 0),
-                                      (n_out, cost("out", N - plan.j, True), lane_offset(n_in, G))])))
+        phases.append(("leaf", phase([(n_in, cost("in", plan.j, plan.f_in, True), 0),
+                                      (n_out, cost("out", N - plan.j, plan.f_out, True), lane_offset(n_in, G))])))
     n_join = plan.n_sets_real * 4 * F["JOIN"]      # padding subsets skip their join
     phases.append(("join", (float(n_join), float(n_join * G))))
     by: dict[str, list[float]] = {}
@@ -167,16 +171,53 @@ def default_hs(N: int) -> int:
     return 2 if N in (7, 9) else 1
 
 
+def group_strides(K: int, F: int, nS: int, nR: int) -> tuple[int, int, int]:
+    """Node strides between node mu and mu + 1 of a grouped task (free photons = the last F of S, helicity-
+    major interior layout: node (S, h) at region + h nS + idx(S); nS / nR = subsets of the task's / parent
+    level): (output, parent through a fixed photon, parent through a free photon)."""
+    return (1 << (K - F + 1)) * nS, (1 << (K - F)) * nR, (1 << (K - F + 1)) * nR
+
+
+def swz_h(h: int) -> int:
+    return (h & ~7) | ((h + (h >> 3)) & 7)
+
+
+def leaf_mu(region: int, h0: int, mu: int, K: int, F: int) -> int:
+    """Leaf offset of node mu of a grouped leaf task (kernel: BGGroupFn leaf store): helicity h0 + mu
+    2^(K-F+1), column swz(h) of the leaf rows starting at region."""
+    return region + 2 * swz_h(h0 + mu * (1 << (K - F + 1)))
+
+
+def task_flops(K: int, F: int, prop: bool) -> int:
+    """FP64 flops of one grouped task (2^F nodes): per node K vertices, the first one plain (V or V_T),
+    the others accumulating (VACC or VACC_T); a vertex is transverse (eps^3 = 0) when its photon is
+    free and its polarisation is 1, which the kernel knows at build time; + S per node."""
+    F_ = FLOPS_BG
+    tot = 0
+    for mu in range(1 << F):
+        for q in range(K):
+            trans = q >= K - F and (mu >> (q - (K - F))) & 1
+            if q == 0 if F == 0 else q == K - F:   # the kernel starts each node with its first free photon
+                tot += F_["V_T"] if trans else F_["V"]
+            else:
+                tot += F_["VACC_T"] if trans else F_["VACC"]
+        tot += F_["S"] if prop else 0
+    return tot
+
+
 def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None,
-                 sp: int | None = None, hs: int | None = None) -> BGPlan:
+                 sp: int | None = None, hs: int | None = None, grp: tuple | None = None) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
     G = 1 << N
     full = (1 << N) - 1
     SP = sp if sp is not None else PITCH_BG.get(N, 10)
+    grp = tuple(grp) if grp is not None else (0, 0, 0, 0, 0)
+    grouped = any(grp)
     if store is None:
         store = default_bg_store(N, j)
+    assert not grouped or store + 1 >= max(j, N - j), "grouped plans store every interior level"
     if hs is None:
         hs = default_hs(N)
     if setb is None:
@@ -217,6 +258,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     cur_slot = [0]
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
     leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL)
+    if grouped:   # leaf buffers of one batch skewed by the out-leaf tasks per subset (16-byte columns): the
+        # quarter warps storing the same columns of several subsets hit distinct bank groups
+        leafb += (2 << max(0, N - j - min(grp[3], N - j) + 1)) % 16
     alloc("PHI", 4 * n_hi * 2, 8)
     alloc("UBL", 4 * n_ho * 2, 8)
     alloc("LEAFX", leafb * (setb - 1) - (lay["UBL"] + 4 * n_ho * 2 - lay["PHI"] - leafb) if setb > 1 else 0, 8)
@@ -250,32 +294,88 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
             slot = cur_slot[0] * math.comb(j if side == "in" else N - j, k)   # this subset's batch slot
             return lay[f"{'SIN' if side == 'in' else 'SOUT'}{k}"] + ((slot + idx) * (1 << (k + 1)) + h) * SP
         idx = (in_idx if side == "in" else out_idx)[k][S]
+        if grouped:   # helicity-major: the nodes of one helicity index are consecutive over the subsets
+            return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (h * math.comb(N, k) + idx) * SP
         return lay[f"{'IN' if side == 'in' else 'OUT'}{k}"] + (idx * (1 << (k + 1)) + h) * SP
 
-    def task(side, S, h, out, mask):
-        """descriptor for node (S, h): sum over i in S of parent (S \\ i) x eps_i."""
-        spin = h & 1
-        lam = {x: (h >> (1 + p)) & 1 for p, x in enumerate(S)}
-        d = [mask, out]
-        for i in S:
-            R = tuple(x for x in S if x != i)
-            d += [node_off(side, R, hel(R, lam, spin)), eps_off(i, lam[i])]
+    def gtask(side, S, F, lf, spin, out_of, mask, leafreg=None):
+        """Grouped task of node set S (sorted) for fixed polarisations lf (of the first K-F photons) and
+        spin: the 2^F nodes mu = polarisations of the LAST F photons of S (helicity bits K-F+1..K).
+        Descriptor [mask, out_0, (parent_0, eps_0) per photon of S, (leaves:) h0]; the kernel steps node mu's
+        output / parents by group_strides() (leaf outputs: leaf_mu(out_0 = region, h0)); free photons'
+        eps(lam = 1) sit 4 doubles after eps(lam = 0).  Every offset the kernel derives is checked here
+        against the plain node layout."""
+        K = len(S)
+        nS = math.comb(N, K)
+        nR = math.comb(N, K - 1) if K > 1 else 0
+        so, sf, sr = group_strides(K, F, nS, nR)
+        lam0 = {x: (lf >> p) & 1 for p, x in enumerate(S[:K - F])}
+        lam0.update({x: 0 for x in S[K - F:]})
+        h0 = hel(S, lam0, spin)
+        d = [mask, out_of(h0) if leafreg is None else leafreg]
+        for q, x in enumerate(S):
+            R = tuple(y for y in S if y != x)
+            d += [node_off(side, R, hel(R, lam0, spin)), eps_off(x, lam0[x])]
+        if leafreg is not None:
+            d.append(h0)
+        for mu in range(1 << F):                 # layout claims of the kernel, node by node
+            lam = dict(lam0)
+            lam.update({x: (mu >> q) & 1 for q, x in enumerate(S[K - F:])})
+            h = hel(S, lam, spin)
+            assert h == h0 + (1 << (K - F + 1)) * mu
+            if leafreg is None:
+                assert out_of(h) == d[1] + so * SP * mu, (S, mu)
+            else:
+                assert out_of(h) == leaf_mu(leafreg, h0, mu, K, F), (S, mu)
+            for p, x in enumerate(S):
+                R = tuple(y for y in S if y != x)
+                par = node_off(side, R, hel(R, lam, spin))
+                if p >= K - F:
+                    q = p - (K - F)
+                    mr = (mu & ((1 << q) - 1)) | ((mu >> (q + 1)) << q)
+                    assert par == d[2 + 2 * p] + sr * SP * mr, (S, mu, p)
+                    assert eps_off(x, lam[x]) == d[3 + 2 * p] + 4 * ((mu >> q) & 1)
+                else:
+                    assert par == d[2 + 2 * p] + sf * SP * mu, (S, mu, p)
+                    assert eps_off(x, lam[x]) == d[3 + 2 * p]
         return d
+
+    def level_tasks(side, Ss, kind, leafreg=None, nh=0):
+        """Tasks of the node sets Ss: ungrouped (F = 0) in the original (S, h) order; grouped in (h0, S)
+        order, so that consecutive lanes take consecutive nodes of the helicity-major layout."""
+        res = []
+        K = len(Ss[0])
+        F = fsel(kind, K)
+        if not grouped:
+            assert F == 0
+        order = [(lf, sp, S) for lf in range(1 << (K - F)) for sp in range(2) for S in Ss] if grouped else \
+            [(lf, sp, S) for S in Ss for lf in range(1 << (K - F)) for sp in range(2)]
+        for lf, spin, S in order:
+            mask = mask_off(msk(S) if side == "in" else full & ~msk(S))
+            if leafreg is None:
+                res.append(gtask(side, S, F, lf, spin, lambda h, S=S: node_off(side, S, h), mask))
+            else:
+                res.append(gtask(side, S, F, lf, spin, lambda h: leaf_off(leafreg, nh, 0, h),
+                                 mask if side == "in" else 0, leafreg if grouped else None))
+        return res
+
+    def fsel(kind: str, k: int) -> int:
+        F = {"lvl": grp[0] if k == 1 else grp[1], "in_leaf": grp[2], "out_leaf": grp[3], "rec": grp[4]}[kind]
+        return min(F, k)
 
     plan = BGPlan(N=N, j=j, G=G, sets=[], layout=lay, stride=stride)
     plan.sp = SP
     plan.setb = setb
     plan.store = store
+    plan.grp = grp
     plan.set_stages = []
     for k in range(1, min(max(j, N - j), store + 1)):
         if k < j:
-            t = [task("in", S, h, node_off("in", S, h), mask_off(msk(S)))
-                 for S in _subsets(N, k) for h in range(1 << (k + 1))]
-            plan.levels.append(("in", k, t))
+            t = level_tasks("in", _subsets(N, k), "lvl")
+            plan.levels.append(("in", k, t, fsel("lvl", k)))
         if k < N - j:
-            t = [task("out", T, h, node_off("out", T, h), mask_off(full & ~msk(T)))
-                 for T in _subsets(N, k) for h in range(1 << (k + 1))]
-            plan.levels.append(("out", k, t))
+            t = level_tasks("out", _subsets(N, k), "lvl")
+            plan.levels.append(("out", k, t, fsel("lvl", k)))
     subsets = list(itertools.combinations(range(N), j))
     if hs == 2:
         # two-half joins (lower.hs_table): subsets containing photon N-1 first, so that the two halves
@@ -284,6 +384,7 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     plan.hs = hs
     plan.n_sets_real = len(subsets)
     subsets += [subsets[-1]] * (-len(subsets) % setb)   # ragged last batch: padding, joins skipped
+    plan.f_in, plan.f_out = fsel("in_leaf", j), fsel("out_leaf", N - j)
     for A in subsets:
         Ac = tuple(x for x in range(N) if x not in A)
         plan.sets.append(A)
@@ -303,20 +404,18 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
                 subs = list(itertools.combinations(A, k))
                 for i, S in enumerate(subs):
                     set_local[("in", S)] = i
-                st.append(("in", k, [task("in", S, h, node_off("in", S, h), mask_off(msk(S)))
-                                     for S in subs for h in range(1 << (k + 1))]))
+                st.append(("in", k, level_tasks("in", subs, "rec"), fsel("rec", k)))
             if k < N - j:
                 subs = list(itertools.combinations(Ac, k))
                 for i, T in enumerate(subs):
                     set_local[("out", T)] = i
-                st.append(("out", k, [task("out", T, h, node_off("out", T, h), mask_off(full & ~msk(T)))
-                                      for T in subs for h in range(1 << (k + 1))]))
+                st.append(("out", k, level_tasks("out", subs, "rec"), fsel("rec", k)))
             stages.append(st)
         plan.set_stages.append(stages)
         lb = (len(plan.sets) - 1) % setb          # leaf buffer of this subset within its batch
         phi0, ubl0 = lay["PHI"] + lb * lay["LEAFB"], lay["UBL"] + lb * lay["LEAFB"]
-        plan.set_in.append([task("in", A, h, leaf_off(phi0, n_hi, 0, h), mask_off(msk(A))) for h in range(n_hi)])
-        plan.set_out.append([task("out", Ac, h, leaf_off(ubl0, n_ho, 0, h), 0) for h in range(n_ho)])
+        plan.set_in.append(level_tasks("in", [A], "in_leaf", phi0, n_hi))
+        plan.set_out.append(level_tasks("out", [Ac], "out_leaf", ubl0, n_ho))
 
     F = FLOPS_BG
     H = 1 << (N + 2)
@@ -328,8 +427,8 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     n_out = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(1, N - j)) + \
         math.comb(N, N - j) * (1 << (N - j + 1)) * vflops(N - j)
     plan.max_k = max(j, N - j)
-    plan.dw = 8 if plan.max_k <= 3 else 16          # descriptor width in ushort
-    rec = sum(len(t) * (vflops(k) + F["S"]) for stages in plan.set_stages for st in stages for _, k, t in st)
+    plan.dw = 8 if plan.max_k <= 3 and not grouped else 16   # descriptor width in ushort (grouped: + h0)
+    rec = sum(len(t) * (vflops(k) + F["S"]) << Fk for stages in plan.set_stages for st in stages for _, k, t, Fk in st)
     stored_rec = sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"])
                      for k in range(store + 1, j)) + \
         sum(math.comb(N, k) * (1 << (k + 1)) * (vflops(k) + F["S"]) for k in range(store + 1, N - j))
@@ -344,4 +443,13 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         "join": math.comb(N, j) * H * F["JOIN"],
         "msq": H * F["ABS2"],
     }
+    if grouped:
+        # the kernel's own count: a free photon's lam = 1 vertex is the transverse form (eps^3 = 0), known
+        # at build time in a grouped task; everything else as above (each node still computed once)
+        plan.flops["currents_in"] = sum(math.comb(N, k) * (1 << (k + 1 - fsel("lvl" if k < j else "in_leaf", k)))
+                                        * task_flops(k, fsel("lvl" if k < j else "in_leaf", k), True)
+                                        for k in range(1, j + 1))
+        plan.flops["currents_out"] = sum(math.comb(N, k) * (1 << (k + 1 - fsel("lvl", k))) * task_flops(k, fsel("lvl", k), True)
+                                         for k in range(1, N - j)) + \
+            math.comb(N, N - j) * (1 << (N - j + 1 - plan.f_out)) * task_flops(N - j, plan.f_out, False)
     return plan

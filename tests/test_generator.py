@@ -237,3 +237,68 @@ def test_register_body_flops_match_the_flop_model():
     # the generic plan minus the transverse-vertex saving (16 flop per eps(k, 2) vertex, half of all vertices)
     assert sum(_flops(2).values()) == make_plan(2).flops_per_point - 16 * 8
     assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36
+
+
+# ---------------------------------------------------------------- grouped Berends-Giele tasks (round 3)
+@pytest.mark.parametrize("N,grp,setb", [(3, (1, 1, 1, 2, 1), 2), (4, (1, 2, 2, 2, 2), 3), (5, (1, 2, 1, 2, 2), 2),
+                                        (5, (1, 2, 2, 2, 2), 5), (6, (1, 2, 1, 1, 1), 4), (7, (1, 1, 1, 1, 1), None)])
+def test_bg_grouped_tasks_interpreted_match_oracle(N, grp, setb):
+    """Grouped tasks (2^F nodes per descriptor, helicity-major interior layout, strided parents, skewed
+    leaf buffers; gen/lower_bg.py gtask) executed by the kernel's offset rules give the oracle's amplitudes."""
+    from paper_2511_19456_b200.gen.interp import eval_point_bg
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    n = N - 1
+    plan = make_bg_plan(N, grp=grp, setb=setb)
+    assert plan.grp == grp and plan.dw == 16
+    mom = synthetic.rambo_cm(n, 2, sqrt_s=5.0, seed=800 + n).numpy()
+    A = oracle.amps(1, n, mom)
+    for k in range(2):
+        B = eval_point_bg(plan, mom[k], 1)
+        assert np.max(np.abs(A[k] - B)) <= 1e-12 * np.max(np.abs(A[k]))
+
+
+def test_bg_grouped_flops_are_generic_minus_transverse():
+    """A grouped task evaluates the same nodes; the only flop difference is the transverse vertex (eps^3 = 0)
+    of each free photon with lam = 1: 40 -> 24 as first vertex, 48 -> 32 accumulating."""
+    import math
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    for N, grp in [(4, (1, 1, 1, 1, 1)), (5, (1, 2, 2, 2, 2)), (6, (1, 2, 1, 1, 1))]:
+        g, u = make_bg_plan(N, grp=grp), make_bg_plan(N)
+        j = g.j
+        saved = 0
+
+        def level_saving(K, F, count_nodes):
+            # per node: half of the nodes have lam = 1 for each free photon; the first free photon's vertex
+            # is the plain one (saves 16), the other free photons' vertices accumulate (save 16)
+            return count_nodes * F * 16 // 2
+
+        for k in range(1, j):
+            saved += level_saving(k, min(grp[0] if k == 1 else grp[1], k), math.comb(N, k) << (k + 1))
+        for k in range(1, N - j):
+            saved += level_saving(k, min(grp[0] if k == 1 else grp[1], k), math.comb(N, k) << (k + 1))
+        saved += level_saving(j, min(grp[2], j), math.comb(N, j) << (j + 1))
+        saved += level_saving(N - j, min(grp[3], N - j), math.comb(N, N - j) << (N - j + 1))
+        assert u.flops_per_point - g.flops_per_point == saved, N
+
+
+def test_bg_grouped_layout_claims_fail_on_a_wrong_stride():
+    """Self-check of the interpreter: a wrong parent stride (what a kernel / table mismatch looks like)
+    breaks the amplitude, so the grouped parity tests above can fail."""
+    from paper_2511_19456_b200.gen import interp
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    plan = make_bg_plan(5, grp=(1, 2, 2, 2, 2), setb=5)
+    mom = synthetic.rambo_cm(4, 1, sqrt_s=5.0, seed=801).numpy()
+    A = oracle.amps(1, 4, mom)
+    orig = interp.expand_group
+
+    def wrong(d, K, F, sp, leaf, N):
+        e = orig(d, K, F, sp, leaf, N)
+        if F and K == 2 and not leaf and len(e) > 1:
+            e[1][2] += sp          # node mu = 1 reads the neighbouring parent
+        return e
+    interp.expand_group = wrong
+    try:
+        B = interp.eval_point_bg(plan, mom[0], 1)
+    finally:
+        interp.expand_group = orig
+    assert np.max(np.abs(A[0] - B)) > 1e-6 * np.max(np.abs(A[0]))

@@ -13,7 +13,7 @@ for item in $SPEC; do
   if [[ $key == bg* ]]; then algo=bg; n=${key#bg}; fi
   for v in ${vs//,/ }; do
     QED_VARIANT=$v timeout 300 python bench.py --n $n --points ${PTS[$n]} --steps 10 --warmup 3 --no-per-n \
-      --no-cpu-baseline --no-e2e --no-mc --algorithm $algo 2>/dev/null | tail -1 | \
+      --no-cpu-baseline --no-e2e --no-mc --no-configs --algorithm $algo 2>>gpurun_out/sweep_${TAG}.err | tail -1 | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print(json.dumps({'n':$n,'algorithm':'$algo','variant':$v,'value':d['value'],'frac':d['roofline']['frac'],'sm_mhz':d['clocks']['sm_mhz'],'kernel':d['config']['kernel']}))" >> $OUT
   done
 done
