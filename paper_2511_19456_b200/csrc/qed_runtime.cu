@@ -40,34 +40,42 @@ void qedgen_config_N6(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N2(int, int);
 const void* qedbg_mc_kernel_N2(int);
 int qedbg_num_variants_N2(void);
+int qedbg_mc_variant_N2(void);
 void qedbg_config_N2(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N3(int, int);
 const void* qedbg_mc_kernel_N3(int);
 int qedbg_num_variants_N3(void);
+int qedbg_mc_variant_N3(void);
 void qedbg_config_N3(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N4(int, int);
 const void* qedbg_mc_kernel_N4(int);
 int qedbg_num_variants_N4(void);
+int qedbg_mc_variant_N4(void);
 void qedbg_config_N4(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N5(int, int);
 const void* qedbg_mc_kernel_N5(int);
 int qedbg_num_variants_N5(void);
+int qedbg_mc_variant_N5(void);
 void qedbg_config_N5(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N6(int, int);
 const void* qedbg_mc_kernel_N6(int);
 int qedbg_num_variants_N6(void);
+int qedbg_mc_variant_N6(void);
 void qedbg_config_N6(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N7(int, int);
 const void* qedbg_mc_kernel_N7(int);
 int qedbg_num_variants_N7(void);
+int qedbg_mc_variant_N7(void);
 void qedbg_config_N7(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N8(int, int);
 const void* qedbg_mc_kernel_N8(int);
 int qedbg_num_variants_N8(void);
+int qedbg_mc_variant_N8(void);
 void qedbg_config_N8(int, int*, int*, long long*, long long*);
 const void* qedbg_kernel_N9(int, int);
 const void* qedbg_mc_kernel_N9(int);
 int qedbg_num_variants_N9(void);
+int qedbg_mc_variant_N9(void);
 void qedbg_config_N9(int, int*, int*, long long*, long long*);
 const void* qedregs_kernel_N2(int, int);
 int qedregs_num_variants_N2(void);
@@ -99,25 +107,26 @@ struct KernelEntry {
   const void* (*mc_kernel)(int);
   void (*config)(int, int*, int*, long long*, long long*);
   int (*num_variants)(void);
+  int (*mc_variant)(void);   // launch variant of the fused MC kernel (nullptr: 0)
 };
 
 const KernelEntry kKernels[] = {
-    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2, qedgen_num_variants_N2},
-    {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3, qedgen_num_variants_N3},
-    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4, qedgen_num_variants_N4},
-    {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5, qedgen_num_variants_N5},
-    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6},
+    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2, qedgen_num_variants_N2, nullptr},
+    {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3, qedgen_num_variants_N3, nullptr},
+    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4, qedgen_num_variants_N4, nullptr},
+    {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5, qedgen_num_variants_N5, nullptr},
+    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6, nullptr},
 };
 
 const KernelEntry kBGKernels[] = {
-    {qedbg_kernel_N2, qedbg_mc_kernel_N2, qedbg_config_N2, qedbg_num_variants_N2},
-    {qedbg_kernel_N3, qedbg_mc_kernel_N3, qedbg_config_N3, qedbg_num_variants_N3},
-    {qedbg_kernel_N4, qedbg_mc_kernel_N4, qedbg_config_N4, qedbg_num_variants_N4},
-    {qedbg_kernel_N5, qedbg_mc_kernel_N5, qedbg_config_N5, qedbg_num_variants_N5},
-    {qedbg_kernel_N6, qedbg_mc_kernel_N6, qedbg_config_N6, qedbg_num_variants_N6},
-    {qedbg_kernel_N7, qedbg_mc_kernel_N7, qedbg_config_N7, qedbg_num_variants_N7},
-    {qedbg_kernel_N8, qedbg_mc_kernel_N8, qedbg_config_N8, qedbg_num_variants_N8},
-    {qedbg_kernel_N9, qedbg_mc_kernel_N9, qedbg_config_N9, qedbg_num_variants_N9},
+    {qedbg_kernel_N2, qedbg_mc_kernel_N2, qedbg_config_N2, qedbg_num_variants_N2, qedbg_mc_variant_N2},
+    {qedbg_kernel_N3, qedbg_mc_kernel_N3, qedbg_config_N3, qedbg_num_variants_N3, qedbg_mc_variant_N3},
+    {qedbg_kernel_N4, qedbg_mc_kernel_N4, qedbg_config_N4, qedbg_num_variants_N4, qedbg_mc_variant_N4},
+    {qedbg_kernel_N5, qedbg_mc_kernel_N5, qedbg_config_N5, qedbg_num_variants_N5, qedbg_mc_variant_N5},
+    {qedbg_kernel_N6, qedbg_mc_kernel_N6, qedbg_config_N6, qedbg_num_variants_N6, qedbg_mc_variant_N6},
+    {qedbg_kernel_N7, qedbg_mc_kernel_N7, qedbg_config_N7, qedbg_num_variants_N7, qedbg_mc_variant_N7},
+    {qedbg_kernel_N8, qedbg_mc_kernel_N8, qedbg_config_N8, qedbg_num_variants_N8, qedbg_mc_variant_N8},
+    {qedbg_kernel_N9, qedbg_mc_kernel_N9, qedbg_config_N9, qedbg_num_variants_N9, qedbg_mc_variant_N9},
 };
 
 // launch variant from QED_VARIANT (tuning experiments); unset = 0 (default); anything that is not an
@@ -297,7 +306,8 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   }
   int mc_wpb = 0, mc_ppw = 0;
   long long mc_smem = 0, mc_flops = 0;
-  ke.config(0, &mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
+  const int mcv = ke.mc_variant ? ke.mc_variant() : 0;
+  ke.config(mcv, &mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
 
   cudaError_t e = cudaGetDevice(&P->device);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaGetDevice"); }
@@ -314,7 +324,7 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   }
   P->grid_blocks = blocks_per_sm * P->num_sms;
   // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
-  P->kern_mc = ke.mc_kernel(0);
+  P->kern_mc = ke.mc_kernel(mcv);
   P->mc_wpb = mc_wpb;
   P->smem_mc = mc_smem + 3LL * 8 * (mc_wpb * 32 / (1 << N));
   e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);

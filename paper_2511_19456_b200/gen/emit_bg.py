@@ -208,6 +208,7 @@ def emit_bg_source(plan: BGPlan, extras: tuple = ()) -> str:
     mcases = "\n".join(f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{ns}::T, {ns}::V{k}>;"
                        for i, (ns, k, _, _) in enumerate(allv))
     n = len(allv)
+    mcv = 1 if (N in PROMOTE and extras) else 0      # the original default plan's V0
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_bg.py -- do not edit.
 // Berends-Giele (distributive rewrite of the node-reduced CDAG, NEXT #1) for N = {N} photons (n = {N - 1}):
 // {plan.n_sets_real} photon subsets A (|A| = j = {plan.j}), one join each, {plan.H} configurations per point.
@@ -217,6 +218,7 @@ def emit_bg_source(plan: BGPlan, extras: tuple = ()) -> str:
 {code}
 extern "C" {{
 int qedbg_num_variants_N{N}(void) {{ return {n}; }}
+int qedbg_mc_variant_N{N}(void) {{ return {mcv}; }}
 const void* qedbg_kernel_N{N}(int per_config, int variant) {{
   switch (variant) {{
 {kcases}
@@ -247,15 +249,22 @@ void qedbg_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, 
 # node-grouped candidate plans (round 3), compiled beside the default as further launch variants and
 # measured with QED_VARIANT (tools/sweep.sh): grp = F per stage kind (level 1, levels >= 2, in-leaf,
 # out-leaf, recomputed), setb = subsets per leaf stage
-# (profiles/sweep_r50, r51: every other candidate measured 20-45 % slower at n = 3, 4, within noise at
-# n = 6 -- the wider tasks leave more lanes idle in each divergent in-/out-leaf phase)
+# (profiles/sweep_r50, r51: every grouped candidate but the n = 5 one measured 20-45 % slower at n = 3, 4 --
+# the wider tasks leave more lanes idle in each divergent in-/out-leaf phase, lower_bg.simt_utilisation);
+# ungrouped candidates with the subset batch the SIMT model prefers (sweep r52)
 CANDIDATES = {
-    6: [dict(grp=(1, 2, 1, 1, 1), setb=4)],
+    5: [dict(setb=4), dict(setb=3)],
+    6: [dict(grp=(1, 2, 1, 1, 1), setb=4), dict(setb=4), dict(setb=6)],
+    7: [dict(setb=5, hs=1)],
 }
 
 
-# (candidate, its variant) promoted to variant 0: n = 5 grouped plan V1 (12 blocks/SM), profiles/sweep_r51
-PROMOTE = {6: (0, 1)}
+# (candidate, its variant) promoted to variant 0 where the sweep measured it faster than the default plan
+# (profiles/sweep_r52_setb.jsonl, B200 at 1965 MHz): n = 4 SETB 4 + descriptor prefetch +3.2 %, n = 5 SETB 4
+# (12 blocks/SM) +8.7 %, n = 6 SETB 5 with one-tile joins +7.2 %; n = 7, 8 candidates (SETB 3, 4, one-tile
+# joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl) and were dropped.  The fused MC kernel keeps
+# the original default plan (qedbg_mc_variant_N*: the promoted n = 4 plan measured 3.7 % slower inside MC)
+PROMOTE = {5: (0, 2), 6: (1, 1), 7: (0, 0)}
 
 
 def candidate_plans(N: int) -> list[dict]:

@@ -126,6 +126,61 @@ def lane_utilisation(plan) -> tuple[float, dict]:
     return sum(a[1] for a in by.values()) / (G * span), by
 
 
+def simt_utilisation(plan) -> tuple[float, dict]:
+    """SIMT-aware variant of lane_utilisation: the task kinds of one phase are different code paths, so a
+    warp runs them one after the other, each for as many trips as its busiest lane needs (idle lanes of a
+    path are lost, not filled by the other kind).  Phase cost = max over the group's warps of the sum over
+    kinds of (trips x task cost).  It explains the round-3 grouped-task measurements (profiles/sweep_r51:
+    n = 4 (1,2,2,2,2)/5 modelled 0.66 of the default's utilisation, measured 0.80 of its rate)."""
+    G, B, N = plan.G, plan.setb, plan.N
+    W = max(1, G // 32)
+
+    def cost(kind, K, F=0, leaf=False):
+        return task_flops(K, F, kind == "in" or not leaf)
+
+    def phase(groups):
+        worst = 0.0
+        for w in range(W):
+            lanes = range(w * 32, min(G, (w + 1) * 32))
+            tot = 0.0
+            for cnt, c, off in groups:
+                trips = max(sum(1 for t in range(cnt) if (t + off) % G == g) for g in lanes)
+                tot += trips * c
+            worst = max(worst, tot)
+        return worst, sum(cnt * c for cnt, c, _ in groups) / W
+
+    phases = []
+    i = 0
+    while i < len(plan.levels):
+        kind, K, t, F0 = plan.levels[i]
+        grp = [(len(t), cost(kind, K, F0), 0)]
+        if i + 1 < len(plan.levels) and plan.levels[i + 1][1] == K:
+            k2, _, t2, F2 = plan.levels[i + 1]
+            grp.append((len(t2), cost(k2, K, F2), lane_offset(len(t), G)))
+            i += 1
+        phases.append(("int", phase(grp)))
+        i += 1
+    for _ in range(len(plan.sets) // B):
+        for st in plan.set_stages[0]:
+            grp, prev = [], 0
+            for q, (kind, K, t, F0) in enumerate(st):
+                grp.append((len(t) * B, cost(kind, K, F0), lane_offset(prev, G) if q > 0 else 0))
+                prev = len(t) * B
+            phases.append(("rec", phase(grp)))
+        n_in, n_out = B * len(plan.set_in[0]), B * len(plan.set_out[0])
+        phases.append(("leaf", phase([(n_in, cost("in", plan.j, plan.f_in, True), 0),
+                                      (n_out, cost("out", N - plan.j, plan.f_out, True), lane_offset(n_in, G))])))
+    n_join = plan.n_sets_real * 4 * FLOPS_BG["JOIN"]
+    phases.append(("join", (float(n_join), float(n_join * min(G, 32)))))
+    by: dict[str, list[float]] = {}
+    for k, (m, w) in phases:
+        a = by.setdefault(k, [0.0, 0.0])
+        a[0] += m
+        a[1] += w
+    span = sum(a[0] for a in by.values())
+    return sum(a[1] for a in by.values()) / (min(G, 32) * span), by
+
+
 # sizes where the GPU sweep overrules the model (profiles/sweep_r18.jsonl: the modelled batch of 2 at
 # n = 2 and of 4 at n = 7 measured 3 % and 6 % slower than 1 and 2)
 SETB_MEASURED = {(3, 1): 1, (8, 4): 2}

@@ -5,7 +5,7 @@ TAG=${1:-r01}
 SPEC=${2:-"2:0,1,2,3,4 1:0,1,2,3,4 3:0,1,2 4:0,1,2 5:0,1,2"}
 OUT=gpurun_out/sweep_${TAG}.jsonl
 mkdir -p gpurun_out; : > $OUT
-declare -A PTS=([1]=4194304 [2]=4194304 [3]=2097152 [4]=1048576 [5]=262144 [6]=262144 [7]=65536 [8]=16384)
+declare -A PTS=([1]=4194304 [2]=4194304 [3]=4194304 [4]=2097152 [5]=1048576 [6]=262144 [7]=65536 [8]=16384)
 # item "n:variants" (CDAG) or "bgN:variants" (Berends-Giele)
 for item in $SPEC; do
   key=${item%%:*}; vs=${item#*:}
