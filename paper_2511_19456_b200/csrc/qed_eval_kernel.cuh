@@ -158,7 +158,7 @@ struct BGFn {  // KIND: 0 in_node, 1 out_node, 2 in_leaf, 3 out_leaf
   }
 };
 
-// ---- grouped Berends-Giele tasks (round 3; gen/lower_bg.py gtask): one descriptor computes the 2^F nodes
+// ---- grouped Berends-Giele tasks (profiles/r03; gen/lower_bg.py gtask): one descriptor computes the 2^F nodes
 // (S, spin, lam_fixed, mu) of one photon set S, mu = the polarisations of the LAST F photons of S (helicity
 // bits K-F+1..K).  Descriptor [mask, out_0, (parent_0, eps_0) per photon p of S, (leaf tasks:) h0] for node
 // mu = 0.  Interior levels are stored helicity-major, so node mu's output and parents sit at fixed strides

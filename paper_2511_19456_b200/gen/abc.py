@@ -32,8 +32,46 @@ def _name(S) -> str:
     return "".join(str(i) for i in S)
 
 
+BATCH_INV_MIN_N = 6   # r54: N = 6 +43 % (CDAG) / +108 % (BG); N = 4 (HBM-bound) -5 % with it
+
+
 def _subset_prelude(N, L):
-    """Q_S and r(S) for every proper non-empty subset, by increasing size (Q_S = Q_{S minus max} + q_max)."""
+    """Q_S and r(S) for every proper non-empty subset, by increasing size (Q_S = Q_{S minus max} + q_max).
+    For N >= BATCH_INV_MIN_N the reciprocals of one size are taken together (Montgomery's batch inversion:
+    prefix products, one division, two multiplications back per subset), so a subset costs 3
+    multiplications instead of an FP64 division (a reciprocal-estimate + Newton sequence, ~8 FP64 pipe
+    operations); the chains of the N - 1 sizes are independent."""
+    if N < BATCH_INV_MIN_N:
+        return _subset_prelude_div(N, L)
+    flops = 0
+    for size in range(1, N):
+        subs = list(itertools.combinations(range(N), size))
+        for S in subs:
+            prev = "pA" if size == 1 else f"Q{_name(S[:-1])}"
+            b = S[-1]
+            L.append(f"  double Q{_name(S)}[4];")
+            L.append(f"  for (int mu = 0; mu < 4; ++mu) Q{_name(S)}[mu] = fma(sg[{b}], k[{b}][mu], {prev}[mu]);")
+            m2 = "kMC2" if size % 2 else "kMA2"
+            q = f"Q{_name(S)}"
+            L.append(f"  const double d{_name(S)} = fma({q}[0], {q}[0], -fma({q}[1], {q}[1], "
+                     f"fma({q}[2], {q}[2], fma({q}[3], {q}[3], {m2}))));")
+            flops += 8 + 8          # 4 fma for Q, 4 fma for D
+        # batch inversion of this size's denominators
+        names = [_name(S) for S in subs]
+        L.append(f"  const double pp{size}_0 = d{names[0]};")
+        for i in range(1, len(names)):
+            L.append(f"  const double pp{size}_{i} = pp{size}_{i - 1} * d{names[i]};")
+        L.append(f"  double iv{size} = 1.0 / pp{size}_{len(names) - 1};")
+        for i in range(len(names) - 1, 0, -1):
+            L.append(f"  const double r{names[i]} = iv{size} * pp{size}_{i - 1};")
+            L.append(f"  iv{size} *= d{names[i]};")
+        L.append(f"  const double r{names[0]} = iv{size};")
+        flops += 3 * (len(names) - 1) + 1
+    return flops
+
+
+def _subset_prelude_div(N, L):
+    """The same with one division per subset (HBM-bound sizes: the serial product chains cost more there)."""
     flops = 0
     for size in range(1, N):
         for S in itertools.combinations(range(N), size):

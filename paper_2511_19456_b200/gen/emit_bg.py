@@ -190,7 +190,7 @@ struct T {{
 
 def emit_bg_source(plan: BGPlan, extras: tuple = ()) -> str:
     """The translation unit of one size: the default plan (variants 0..) and candidate plans `extras`
-    (node-grouped, round 3) appended as further launch variants."""
+    (node-grouped, profiles/r03) appended as further launch variants."""
     N = plan.N
     code, allv = emit_bg_ns(plan, f"qedbg_N{N}")
     for i, p in enumerate(extras):
@@ -246,7 +246,7 @@ void qedbg_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, 
 """
 
 
-# node-grouped candidate plans (round 3), compiled beside the default as further launch variants and
+# node-grouped candidate plans (profiles/r03), compiled beside the default as further launch variants and
 # measured with QED_VARIANT (tools/sweep.sh): grp = F per stage kind (level 1, levels >= 2, in-leaf,
 # out-leaf, recomputed), setb = subsets per leaf stage
 # (profiles/sweep_r50, r51: every grouped candidate but the n = 5 one measured 20-45 % slower at n = 3, 4 --

@@ -50,7 +50,7 @@ class BGPlan:
     flops: dict[str, int] = field(default_factory=dict)
     n_sets_real: int = 0     # C(N, j); sets[n_sets_real:] pad the last batch to SETB subsets
     hs: int = 1              # join halves (lower.hs_table): 1 = lane tile (s, s'); 2 = (s, s', lam_{N-1})
-    # node groups (round 3): F free polarisation bits per task of each stage kind; a task computes the 2^F
+    # node groups (profiles/r03): F free polarisation bits per task of each stage kind; a task computes the 2^F
     # nodes (S, spin, lam_fixed, mu) of one subset S, mu = the polarisations of the first F photons of S
     grp: tuple = (0, 0, 0, 0, 0)   # (level 1, levels >= 2, in-leaf, out-leaf, recomputed levels)
 
