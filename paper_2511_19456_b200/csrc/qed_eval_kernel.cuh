@@ -54,6 +54,16 @@ __device__ __forceinline__ void ld_mask(const double* p, double (&m)[5]) {
   m[0] = a.x; m[1] = a.y; m[2] = b.x; m[3] = b.y; m[4] = p[4];
 }
 
+// plans with tensor-core joins define MMA = true (gen/emit.py); every other traits struct reads false
+template <class T, class = void>
+struct mma_of {
+  static constexpr bool value = false;
+};
+template <class T>
+struct mma_of<T, decltype(void(T::MMA))> {
+  static constexpr bool value = T::MMA;
+};
+
 // ---- task kinds (one trie node x one helicity state); descriptor = (parent, eps, mask, out)
 template <class T>
 struct Tasks {
@@ -76,13 +86,17 @@ struct Tasks {
     double e[3], m[5];
     ld_eps(b + t.y, e);
     ld_mask(b + t.z, m);
-    st_leaf<T::NHI>(b + t.w, prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x))));
+    const spinor v = prop_col(m, eslash_col(e, ld_aos<T::SP>(b, t.x)));
+    if constexpr (mma_of<T>::value) st_aos<8>(b, t.w, v);   // tensor-core joins: AoS leaves (64-byte pitch, XOR swizzle)
+    else st_leaf<T::NHI>(b + t.w, v);
   }
   // out-side leaf: ubar = parent epsslash
   static __device__ __forceinline__ void ub(double* b, ushort4 t) {
     double e[3];
     ld_eps(b + t.y, e);
-    st_leaf<T::NHO>(b + t.w, eslash_row(e, ld_aos<T::SP>(b, t.x)));
+    const spinor v = eslash_row(e, ld_aos<T::SP>(b, t.x));
+    if constexpr (mma_of<T>::value) st_aos<8>(b, t.w, v);
+    else st_leaf<T::NHO>(b + t.w, v);
   }
 };
 
@@ -486,6 +500,112 @@ __device__ __forceinline__ void join_set_hs(const double* __restrict__ base, uin
   }
 }
 
+// ---- tensor-core joins (T::MMA; gen/lower.py make_plan(mma=True)).  For one photon subset A the joins of
+// all (sigma, tau) diagrams over every configuration are complex matrix products
+//   C[row][col] += sum_c ubar_tau[row][c] phi_sigma[col][c],
+// rows = (s', lam of the complement's photons), cols = (s, lam of A's photons), run on the FP64 tensor core
+// as DMMA m8n8k4 (4 per 8 x 8 tile: C_re += U_re P_re - U_im P_im, C_im += U_re P_im + U_im P_re).  DMMA and
+// DFMA share one FP64 datapath on B200 (tools/micro/dmma_peak.cu: 37.1 TF/s alone, the serial sum
+// together), but a DMMA carries 512 flop per warp instruction from 2 register operands per lane, so the
+// join needs 1/8 of the issue slots and half the shared-memory wavefronts of the CUDA-core join.
+// Fragment layout (tools/micro/dmma_layout.cu): lane t holds A[t >> 2][t & 3], B[t & 3][t >> 2] and
+// C[t >> 2][2 (t & 3) + r].  Accumulator bits: row = lane bits 2..4 (+ tile TR), col = r, lane bits 0..1
+// (+ tile TC); which photon's polarisation sits on which bit depends on the subset and changes by one
+// exchange of two bits between consecutive subsets (Johnson order, T::mma_swap).
+struct MmaAcc {
+  double re[2], im[2];
+};
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+template <class T>
+struct Mma {
+  static constexpr int TR = T::NHO / 8 > 0 ? T::NHO / 8 : 1, TC = T::NHI / 8 > 0 ? T::NHI / 8 : 1;
+  static constexpr int P = T::G < 32 ? 32 / T::G : 1;   // points per warp
+};
+// joins of sigma rows [sg0, sg1) of the point whose slot is pbase into acc
+template <class T>
+__device__ __forceinline__ void join_mma(const double* __restrict__ pbase, int lane, int sg0, int sg1,
+                                         MmaAcc (&acc)[Mma<T>::TR][Mma<T>::TC]) {
+  constexpr int TR = Mma<T>::TR, TC = Mma<T>::TC;
+  const int ri = lane >> 2, c = lane & 3;
+#pragma unroll 1
+  for (int sg = sg0; sg < sg1; ++sg) {
+    double bre[TC], bim[TC];
+#pragma unroll
+    for (int tc = 0; tc < TC; ++tc) {
+      const c2 v = ld2(pbase + aos_slot<8>(T::PHI + (sg * T::NHI + tc * 8 + ri) * 8, c));
+      bre[tc] = v.r;
+      bim[tc] = v.i;
+    }
+#pragma unroll 2
+    for (int tu = 0; tu < T::NTAU; ++tu) {
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr) {
+        const c2 u = ld2(pbase + aos_slot<8>(T::UBL + (tu * T::NHO + tr * 8 + ri) * 8, c));
+        const double nui = -u.i;
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc) {
+          dmma(acc[tr][tc].re[0], acc[tr][tc].re[1], u.r, bre[tc]);
+          dmma(acc[tr][tc].im[0], acc[tr][tc].im[1], u.r, bim[tc]);
+          dmma(acc[tr][tc].re[0], acc[tr][tc].re[1], nui, bim[tc]);
+          dmma(acc[tr][tc].im[0], acc[tr][tc].im[1], u.i, bre[tc]);
+        }
+      }
+    }
+  }
+}
+// exchanges of two accumulator bits (T::mma_swap, generated): lane bit A <-> lane bit B
+template <int A, int B, int TR, int TC>
+__device__ __forceinline__ void mma_swap_ll(MmaAcc (&acc)[TR][TC], int lane) {
+  const int src = (lane & ~((1 << A) | (1 << B))) | (((lane >> A) & 1) << B) | (((lane >> B) & 1) << A);
+#pragma unroll
+  for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        acc[tr][tc].re[r] = __shfl_sync(0xffffffffu, acc[tr][tc].re[r], src);
+        acc[tr][tc].im[r] = __shfl_sync(0xffffffffu, acc[tr][tc].im[r], src);
+      }
+}
+// lane bit A <-> tile index bit (ROW: the row tile TR, else the column tile TC)
+template <int A, bool ROW, int TR, int TC>
+__device__ __forceinline__ void mma_swap_lt(MmaAcc (&acc)[TR][TC], int lane) {
+  const int la = (lane >> A) & 1;
+  MmaAcc o[TR][TC];
+#pragma unroll
+  for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < TC; ++tc) o[tr][tc] = acc[tr][tc];
+#pragma unroll
+  for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+    for (int tc = 0; tc < TC; ++tc) {
+      const int t = ROW ? tr : tc;            // the new element's tile bit = the source lane's bit A
+      const int src = (lane & ~(1 << A)) | (t << A);
+      const MmaAcc& s0 = ROW ? o[0][tc] : o[tr][0];
+      const MmaAcc& s1 = ROW ? o[TR - 1][tc] : o[tr][TC - 1];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const double x0 = __shfl_sync(0xffffffffu, s0.re[r], src), x1 = __shfl_sync(0xffffffffu, s1.re[r], src);
+        const double y0 = __shfl_sync(0xffffffffu, s0.im[r], src), y1 = __shfl_sync(0xffffffffu, s1.im[r], src);
+        acc[tr][tc].re[r] = la ? x1 : x0;
+        acc[tr][tc].im[r] = la ? y1 : y0;
+      }
+    }
+}
+// column tile <-> row tile
+template <int TR, int TC>
+__device__ __forceinline__ void mma_swap_tt(MmaAcc (&acc)[TR][TC]) {
+  static_assert(TR == 2 && TC == 2, "tile exchange needs both tile bits");
+  const MmaAcc t = acc[0][1];
+  acc[0][1] = acc[1][0];
+  acc[1][0] = t;
+}
+
 // Stages 1-3 for the point whose momenta are in base[T::MOM..].  On return lane g holds the
 // amplitudes (without e^N) of its configurations in amp[s | s' << 1] (re, im).
 // launch-variant field DP (descriptor prefetch; plans that emit T::SD); variants without the field read 0
@@ -511,6 +631,7 @@ struct sd_of<T, true> {
 // DP: leaf-stage descriptors loaded one subset (batch) ahead (T::SD / load_set / run_set_d)
 template <class T, int AS = 2, int SB = 1, int DP = 0>
 __device__ __forceinline__ void eval_point(double* base, int g, int pb, const QedEvalArgs& a, double (&amp)[2 * T::NAMP]) {
+  static_assert(!mma_of<T>::value, "tensor-core-join plans run mma_eval");
   stage_externals<T>(base, g, a);
   group_sync<T>(pb);
   T::run_interiors(base, g, pb);
@@ -640,6 +761,113 @@ __device__ __forceinline__ double group_msq(const double (&amp)[2 * T::NAMP], in
   return a.norm * sum;
 }
 
+// Stages 1-4 of a tensor-core-join plan for the points of this warp (after stage 0).  Groups of G <= 32 lanes
+// run their own point's tasks; the joins are warp-wide, one point after the other (P per warp).  A 64-lane
+// group splits the sigma rows between its two warps and sums the halves through shared memory.
+template <class T, class V, bool PER_CONFIG>
+__device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int pb, const QedEvalArgs& a, long long p0) {
+  constexpr int TR = Mma<T>::TR, TC = Mma<T>::TC, P = Mma<T>::P;
+  constexpr int DP = dp_of<V>::value;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  stage_externals<T>(base, g, a);
+  group_sync<T>(pb);
+  T::run_interiors(base, g, pb);
+  MmaAcc acc[P][TR][TC];
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+      for (int tc = 0; tc < TC; ++tc) acc[p][tr][tc] = MmaAcc{{0.0, 0.0}, {0.0, 0.0}};
+  const int half = T::G > 32 ? (threadIdx.x >> 5) & 1 : 0;
+  const int sg0 = T::G > 32 ? half * (T::NSIG / 2) : 0, sg1 = T::G > 32 ? sg0 + T::NSIG / 2 + (half ? T::NSIG % 2 : 0) : T::NSIG;
+  typename sd_of<T, DP != 0>::type sd;
+  if constexpr (DP) T::load_set(sd, g, 0);
+#pragma unroll 1
+  for (int si = 0; si < T::NSETS; ++si) {
+    if constexpr (DP) {
+      T::run_set_d(base, g, pb, sd);
+      group_sync<T>(pb);
+      if (si + 1 < T::NSETS) T::load_set(sd, g, si + 1);
+    } else {
+      T::run_set(base, g, pb, si);
+      group_sync<T>(pb);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const double* pbase = T::G > 32 ? base : smem + (w * P + p) * T::STRIDE;
+      join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
+      if (si + 1 < T::NSETS) T::mma_swap(acc[p], lane, si);
+    }
+    group_sync<T>(pb);
+  }
+  if constexpr (T::G > 32) {   // second warp's partial tiles -> the (dead) leaf rows of the point, summed by the first
+    double* red = base + T::PHI;
+    if (half == 1) {
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            red[((tr * TC + tc) * 4 + r) * 32 + lane] = acc[0][tr][tc].re[r];
+            red[((tr * TC + tc) * 4 + 2 + r) * 32 + lane] = acc[0][tr][tc].im[r];
+          }
+    }
+    group_sync<T>(pb);
+    if (half == 0) {
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            acc[0][tr][tc].re[r] += red[((tr * TC + tc) * 4 + r) * 32 + lane];
+            acc[0][tr][tc].im[r] += red[((tr * TC + tc) * 4 + 2 + r) * 32 + lane];
+          }
+    }
+  }
+  // stage 4: |amp|^2 per configuration (config of each accumulator element: T::mma_config)
+  const long long n = a.n_points;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const long long ptp = T::G > 32 ? p0 + pb : p0 + w * P + p;
+    if (PER_CONFIG) {
+      if (ptp < n && half == 0) {
+#pragma unroll
+        for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+          for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const unsigned h = T::mma_config(lane, r, tr, tc);
+              unsigned hx = 0;
+#pragma unroll
+              for (int b = 0; b < T::N + 2; ++b) hx |= ((h >> b) & 1u) << ((a.ext_bit >> (4 * b)) & 15);
+              const double re = acc[p][tr][tc].re[r], im = acc[p][tr][tc].im[r];
+              a.out[ptp * (1LL << (T::N + 2)) + hx] = a.coupling * fma(re, re, im * im);
+            }
+      }
+    } else {
+      double sum = 0.0;
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr)
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const unsigned h = T::mma_config(lane, r, tr, tc);
+            const double re = acc[p][tr][tc].re[r], im = acc[p][tr][tc].im[r];
+            sum += ((h & a.fixed_mask) == a.fixed_val) ? fma(re, re, im * im) : 0.0;
+          }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (ptp < n && half == 0 && (T::G > 32 ? lane == 0 : lane == p * T::G)) a.out[ptp] = a.norm * sum;
+    }
+  }
+}
+
 // V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, AS accumulator split, PF prefetch)
 template <class T, class V, bool PER_CONFIG>
 __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(QedEvalArgs a) {
@@ -686,6 +914,9 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
       }
     }
     group_sync<T>(pb);
+    if constexpr (mma_of<T>::value) {
+      mma_eval<T, V, PER_CONFIG>(smem, base, g, pb, a, p0);
+    } else {
     double amp[2 * T::NAMP];
     eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
     // stage 4: |amp|^2 and the spin/polarisation sum or average
@@ -703,6 +934,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
     } else {
       const double msq = group_msq<T>(amp, g, pb, base, a);
       if (valid && g == 0) a.out[pt] = msq;
+    }
     }
     group_sync<T>(pb);   // the slot is reused by the next point
   }

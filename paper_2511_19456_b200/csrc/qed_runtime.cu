@@ -24,14 +24,19 @@ const void* qedgen_kernel_N5(int, int);
 const void* qedgen_kernel_N6(int, int);
 const void* qedgen_mc_kernel_N2(int);
 int qedgen_num_variants_N2(void);
+int qedgen_mc_variant_N2(void);
 const void* qedgen_mc_kernel_N3(int);
 int qedgen_num_variants_N3(void);
+int qedgen_mc_variant_N3(void);
 const void* qedgen_mc_kernel_N4(int);
 int qedgen_num_variants_N4(void);
+int qedgen_mc_variant_N4(void);
 const void* qedgen_mc_kernel_N5(int);
 int qedgen_num_variants_N5(void);
+int qedgen_mc_variant_N5(void);
 const void* qedgen_mc_kernel_N6(int);
 int qedgen_num_variants_N6(void);
+int qedgen_mc_variant_N6(void);
 void qedgen_config_N2(int, int*, int*, long long*, long long*);
 void qedgen_config_N3(int, int*, int*, long long*, long long*);
 void qedgen_config_N4(int, int*, int*, long long*, long long*);
@@ -111,11 +116,11 @@ struct KernelEntry {
 };
 
 const KernelEntry kKernels[] = {
-    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2, qedgen_num_variants_N2, nullptr},
-    {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3, qedgen_num_variants_N3, nullptr},
-    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4, qedgen_num_variants_N4, nullptr},
-    {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5, qedgen_num_variants_N5, nullptr},
-    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6, nullptr},
+    {qedgen_kernel_N2, qedgen_mc_kernel_N2, qedgen_config_N2, qedgen_num_variants_N2, qedgen_mc_variant_N2},
+    {qedgen_kernel_N3, qedgen_mc_kernel_N3, qedgen_config_N3, qedgen_num_variants_N3, qedgen_mc_variant_N3},
+    {qedgen_kernel_N4, qedgen_mc_kernel_N4, qedgen_config_N4, qedgen_num_variants_N4, qedgen_mc_variant_N4},
+    {qedgen_kernel_N5, qedgen_mc_kernel_N5, qedgen_config_N5, qedgen_num_variants_N5, qedgen_mc_variant_N5},
+    {qedgen_kernel_N6, qedgen_mc_kernel_N6, qedgen_config_N6, qedgen_num_variants_N6, qedgen_mc_variant_N6},
 };
 
 const KernelEntry kBGKernels[] = {

@@ -11,7 +11,46 @@ from __future__ import annotations
 
 import os
 
-from .lower import Plan, hiho_table, lane_offset, make_plan
+from .lower import MMA_COL_POS, MMA_ROW_POS, Plan, hiho_table, lane_offset, make_plan
+
+_LANE_BIT = {"L0": 0, "L1": 1, "L3": 3, "L4": 4}
+
+
+def _mma_members(plan: Plan) -> str:
+    """Traits members of a tensor-core-join plan: MMA, the accumulator bit exchange after each subset
+    (lower.mma_assignments) and the configuration of each accumulator element in the final layout."""
+    cases = []
+    for si, (pa, pc) in enumerate(plan.mma_swaps):
+        if pa in _LANE_BIT and pc in _LANE_BIT:
+            call = f"qed::mma_swap_ll<{_LANE_BIT[pa]}, {_LANE_BIT[pc]}>(acc, lane)"
+        elif pa in _LANE_BIT and pc == "TR":
+            call = f"qed::mma_swap_lt<{_LANE_BIT[pa]}, true>(acc, lane)"
+        elif pa == "TC" and pc in _LANE_BIT:
+            call = f"qed::mma_swap_lt<{_LANE_BIT[pc]}, false>(acc, lane)"
+        else:
+            assert (pa, pc) == ("TC", "TR"), (pa, pc)
+            call = "qed::mma_swap_tt(acc)"
+        cases.append(f"      case {si}: {call}; break;")
+    bit = {"L0": "(lane & 1)", "L1": "((lane >> 1) & 1)", "L3": "((lane >> 3) & 1)", "L4": "((lane >> 4) & 1)",
+           "TR": "tr", "TC": "tc"}
+    terms = [f"((unsigned){bit[pos]} << {1 + x})" for x, pos in sorted(plan.mma_assign[-1].items())]
+    cfg = " | ".join(["(unsigned)r", f"((unsigned)((lane >> 2) & 1) << {plan.N + 1})"] + terms)
+    return f"""  // tensor-core joins (gen/lower.py make_plan(mma=True)): subsets in Johnson order; after subset si the two
+  // accumulator bits whose photons changed sides are exchanged; mma_config = the configuration of element
+  // (lane, r, row tile, column tile) in the final layout
+  static constexpr bool MMA = true;
+  template <class ACC>
+  static __device__ __forceinline__ void mma_swap(ACC& acc, int lane, int si) {{
+    switch (si) {{
+{chr(10).join(cases)}
+      default: break;
+    }}
+  }}
+  static __device__ __forceinline__ unsigned mma_config(int lane, int r, int tr, int tc) {{
+    (void)tr; (void)tc;
+    return {cfg};
+  }}
+"""
 
 SMEM_PER_SM = 228 * 1024
 SMEM_RESERVED_PER_BLOCK = 1024
@@ -157,6 +196,7 @@ struct T {{
   static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = NSETS, SETB = 1, LEAFB = 0;
   static constexpr int HS = 1, NAMP = 4;
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
+{_mma_members(plan) if getattr(plan, "mma", False) else ""}
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
   static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
@@ -181,12 +221,23 @@ struct T {{
 """
 
 
+# tensor-core-join variant promoted to variant 0 (index among the mma variants), where measured faster
+# (profiles/sweep_r55_mma.jsonl: n = 3 +17 %, n = 4 +19 %, n = 5 +24 % over the CUDA-core join, with the
+# descriptor prefetch)
+MMA_PROMOTE: dict[int, int] = {4: 0, 5: 0, 6: 0}
+
+
 def plan_variants(N: int) -> list[Plan]:
     """Lowered plans compiled for one process size: the default, plus (n = 4) one that recomputes the
-    second out-side trie level per subset (22 KB -> 15 KB of shared memory per point)."""
+    second out-side trie level per subset (22 KB -> 15 KB of shared memory per point), plus (n = 3..5) the
+    tensor-core-join plan (make_plan(mma=True))."""
     plans = [make_plan(N)]
+    if N in (4, 5, 6):
+        plans.append(make_plan(N, mma=True))
     if N == 5:
         plans.append(make_plan(N, store=1))
+        # tensor-core joins with less shared memory per point (more resident points): sweep r56
+        plans += [make_plan(N, mma=True, store=1), make_plan(N, mma=True, store=1, sp=8), make_plan(N, mma=True, sp=8)]
         # (r38: the 64-byte spinor pitch, 22 KB per point and 10 resident points per SM, measured 11-16 % slower)
     return plans
 
@@ -197,7 +248,16 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
     nss = [f"qedgen_N{N}"] + [f"qedgen_N{N}_p{i}" for i in range(1, len(plans))]
     vs = []   # (plan index, wpb, min blocks, AS, PF)
     for pi, p in enumerate(plans):
-        vs += [(pi,) + v for v in variants(p)]
+        if getattr(p, "mma", False):   # tensor-core joins: no accumulator split / sigma blocking; +- descriptor prefetch
+            wpb, mb = choose_launch(p)
+            vs += [(pi, wpb, mb, 2, 2, 1, 1), (pi, wpb, mb, 2, 2, 1, 0)]
+        else:
+            vs += [(pi,) + v for v in variants(p)]
+    mma_v = [i for i, v in enumerate(vs) if getattr(plans[v[0]], "mma", False)]
+    if N in MMA_PROMOTE and mma_v:
+        k = mma_v[MMA_PROMOTE[N]]
+        vs = [vs[k]] + vs[:k] + vs[k + 1:]
+    mc_v = next(i for i, v in enumerate(vs) if not getattr(plans[v[0]], "mma", False))
     fl = plan.flops
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     bodies = "\n".join(emit_plan_namespace(p, ns) for p, ns in zip(plans, nss))
@@ -208,8 +268,10 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, false>;"
         for i, (pi, *_) in enumerate(vs))
+    # the fused MC kernel runs the CUDA-core joins (mc_variant): tensor-core variants map to that one
     mc_cases = "\n".join(
-        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{nss[pi]}::T, {nss[pi]}::V{i}>;"
+        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{nss[vs[mc_v if getattr(plans[pi], 'mma', False) else i][0]]}::T, "
+        f"{nss[vs[mc_v if getattr(plans[pi], 'mma', False) else i][0]]}::V{mc_v if getattr(plans[pi], 'mma', False) else i}>;"
         for i, (pi, *_) in enumerate(vs))
     strides = ", ".join(str(plans[pi].stride) for pi, *_ in vs)
     flops = ", ".join(f"{plans[pi].flops_per_point}LL" for pi, *_ in vs)
@@ -227,6 +289,7 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
 {variant_structs}
 extern "C" {{
 int qedgen_num_variants_N{N}(void) {{ return {len(vs)}; }}
+int qedgen_mc_variant_N{N}(void) {{ return {mc_v}; }}
 const void* qedgen_kernel_N{N}(int per_config, int variant) {{
   switch (variant) {{
 {kernel_cases}

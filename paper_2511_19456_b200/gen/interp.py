@@ -68,6 +68,49 @@ def _join_offsets_hs(tab, plan, si, h):
     return (wp >> (8 * s)) & 255, (wu >> (8 * (2 * lx + sp))) & 255
 
 
+MMA_BIT = {"L0": ("col", 1), "L1": ("col", 2), "TC": ("col", 3), "L3": ("row", 1), "L4": ("row", 2), "TR": ("row", 3)}
+
+
+def _mma_join(plan, sm, run, get_aos_sp8):
+    """The tensor-core join of qed_eval_kernel.cuh (join_mma) on one point: per subset (Johnson order),
+    C[row][col] += sum_c ubar_tau[row][c] phi_sigma[col][c] over every diagram (sigma, tau), with rows / cols
+    the accumulator-layout slots (lower.mma_slot); between subsets the accumulator bits of the exchanged
+    positions are swapped (mma_swap); at the end the last subset's assignment maps (row, col) to the
+    configuration.  Returns amplitudes in the internal index (s | lam_i << (1+i) | s' << (N+1))."""
+    N, L = plan.N, plan.layout
+    R, C = plan.n_ho, plan.n_hi
+    acc = np.zeros((R, C), dtype=complex)
+    for si, A in enumerate(plan.sets):
+        for stage in plan.set_stages[si]:
+            for kind, tasks in stage:
+                run(kind, tasks)
+        U = np.array([[get_aos_sp8(L["UBL"] + (t * R + r) * 8) for r in range(R)] for t in range(plan.n_tau)])
+        P = np.array([[get_aos_sp8(L["PHI"] + (s_ * C + c) * 8) for c in range(C)] for s_ in range(plan.n_sigma)])
+        for t in range(plan.n_tau):
+            for s_ in range(plan.n_sigma):
+                acc += U[t] @ P[s_].T
+        if si + 1 < len(plan.sets):
+            pa, pc = plan.mma_swaps[si]
+            (_, ba), (_, bc) = MMA_BIT[pa], MMA_BIT[pc]
+            new = np.empty_like(acc)
+            for r in range(R):
+                for c in range(C):
+                    r2 = (r & ~(1 << bc)) | (((c >> ba) & 1) << bc)
+                    c2 = (c & ~(1 << ba)) | (((r >> bc) & 1) << ba)
+                    new[r][c] = acc[r2][c2]
+            acc = new
+    assign = plan.mma_assign[-1]
+    amp = np.zeros(plan.H, dtype=complex)
+    for r in range(R):
+        for c in range(C):
+            h = (c & 1) | ((r & 1) << (N + 1))
+            for x, pos in assign.items():
+                side, b = MMA_BIT[pos]
+                h |= (((c if side == "col" else r) >> b) & 1) << (1 + x)
+            amp[h] = acc[r][c]
+    return amp
+
+
 def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     """All helicity amplitudes (external bit order, with e^N) at one point, via the tables."""
     N, L = plan.N, plan.layout
@@ -82,6 +125,11 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         return np.array([complex(sm[aos_slot(off, c, plan.sp)], sm[aos_slot(off, c, plan.sp) + 1]) for c in range(4)])
 
     def put_leaf(nh, off, v):     # off: the descriptor's leaf offset (component 0)
+        if getattr(plan, "mma", False):   # AoS leaves, 64-byte pitch with the XOR swizzle
+            for c in range(4):
+                o = aos_slot(off, c, 8)
+                sm[o], sm[o + 1] = v[c].real, v[c].imag
+            return
         for c in range(4):
             o = off + c * nh * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
@@ -141,7 +189,10 @@ def eval_point(plan: Plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
         run("vs_row", tasks)
     H = plan.H
     amp = np.zeros(H, dtype=complex)      # internal index: s | lam_i << (1+i) | s' << (N+1)
-    for si, A in enumerate(plan.sets):
+    if getattr(plan, "mma", False):
+        amp = _mma_join(plan, sm, run, get_aos_sp8=lambda off: np.array(
+            [complex(sm[aos_slot(off, c, 8)], sm[aos_slot(off, c, 8) + 1]) for c in range(4)]))
+    for si, A in enumerate(plan.sets if not getattr(plan, "mma", False) else []):
         for stage in plan.set_stages[si]:
             for kind, tasks in stage:
                 run(kind, tasks)

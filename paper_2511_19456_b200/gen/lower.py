@@ -134,7 +134,58 @@ def default_store(N: int, j: int) -> int:
     return 1 if N >= 6 else max(j, N - j)
 
 
-def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | None = None) -> Plan:
+def johnson_order(N: int, j: int) -> list[tuple[int, ...]]:
+    """The j-subsets of range(N) in an order where consecutive subsets differ by exchanging one element
+    (a Hamiltonian path of the Johnson graph, found by depth-first search; it exists for every N, j)."""
+    subs = list(itertools.combinations(range(N), j))
+    n = len(subs)
+    adj = {a: [b for b in subs if len(set(a) & set(b)) == j - 1] for a in subs}
+    path, seen = [subs[0]], {subs[0]}
+
+    def dfs():
+        if len(path) == n:
+            return True
+        for b in adj[path[-1]]:
+            if b not in seen:
+                seen.add(b)
+                path.append(b)
+                if dfs():
+                    return True
+                path.pop()
+                seen.discard(b)
+        return False
+    assert dfs()
+    return path
+
+
+# tensor-core join (DMMA m8n8k4 f64) physical positions of the photons' polarisation bits in the accumulator
+# layout: the in-set A's photons take the column positions, the complement's the row positions
+MMA_COL_POS = ("L0", "L1", "TC")      # lane bit 0, lane bit 1, column-tile index
+MMA_ROW_POS = ("L3", "L4", "TR")      # lane bit 3, lane bit 4, row-tile index
+
+
+def mma_assignments(N: int, j: int, order: list[tuple[int, ...]]):
+    """Photon -> physical position for every subset of `order`, and the position pair exchanged at each
+    transition.  The first subset assigns sorted photons to positions in order; at a transition the photon
+    entering A takes the position of the photon leaving it and vice versa, so the accumulators of every
+    configuration move by one exchange of two physical bits (qed_eval_kernel.cuh mma_swap)."""
+    assert j <= len(MMA_COL_POS) and N - j <= len(MMA_ROW_POS)
+    A0 = order[0]
+    Ac0 = tuple(x for x in range(N) if x not in A0)
+    cur = {x: MMA_COL_POS[k] for k, x in enumerate(A0)}
+    cur.update({x: MMA_ROW_POS[k] for k, x in enumerate(Ac0)})
+    assigns, swaps = [dict(cur)], []
+    for a, b in zip(order, order[1:]):
+        (out_,), (in_,) = set(a) - set(b), set(b) - set(a)
+        pa, pc = cur[out_], cur[in_]
+        cur[out_], cur[in_] = pc, pa
+        assigns.append(dict(cur))
+        swaps.append((pa, pc))
+    return assigns, swaps
+
+
+def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | None = None,
+              mma: bool = False) -> Plan:
     if N < 2:
         raise ValueError("need at least two photons (n >= 1)")
     if j is None:
@@ -180,8 +231,12 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
         alloc(f"SOUT{i}", perm_count(N - j, i) * (1 << (i + 1)) * SP, 8)
     n_sigma, n_tau = math.factorial(j), math.factorial(N - j)
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
-    alloc("PHI", n_sigma * 4 * n_hi * 2, 8)
-    alloc("UBL", n_tau * 4 * n_ho * 2, 8)
+    if mma:   # AoS leaves (64-byte pitch, XOR component swizzle): spinor (row, slot) at row * NH + slot
+        alloc("PHI", n_sigma * n_hi * 8, 8)
+        alloc("UBL", n_tau * n_ho * 8, 8)
+    else:
+        alloc("PHI", n_sigma * 4 * n_hi * 2, 8)
+        alloc("UBL", n_tau * 4 * n_ho * 2, 8)
     stride = off
     # odd number of 16-byte slots per point: consecutive points of a warp start in different banks
     stride = (stride + 1) // 2 * 2
@@ -203,6 +258,22 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
 
     plan = Plan(N=N, j=j, G=G, store=store, sets=[], sigmas=[], taus=[], layout=lay, stride=stride)
     plan.sp = SP
+    plan.mma = mma
+    order = johnson_order(N, j) if mma else list(itertools.combinations(range(N), j))
+    if mma:
+        plan.mma_assign, plan.mma_swaps = mma_assignments(N, j, order)
+
+    def mma_slot(assign, side_photons, h, prim):
+        """Accumulator-layout index of leaf helicity h (bit 0 = s / s', bit 1 + k = lam of the k-th sorted
+        photon of the side): bit 0 <- the spin, bit 1 <- the photon at L0 / L3, bit 2 <- L1 / L4, bit 3 <- the
+        tile index TC / TR."""
+        slot = h & 1
+        for k, x in enumerate(side_photons):
+            lam = (h >> (1 + k)) & 1
+            p_ = assign[x]
+            bit = {prim[0]: 1, prim[1]: 2, prim[2]: 3}[p_]
+            slot |= lam << bit
+        return slot
 
     # ---------------------------------------------------------------- stored interior levels (V+S1 fused)
     def in_off(prefix, h, set_local=None):
@@ -234,7 +305,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
 
     # ---------------------------------------------------------------- per-set stages
     n_set_in_int = n_set_out_int = 0
-    for A in itertools.combinations(range(N), j):
+    for si_, A in enumerate(order):
         Ac = tuple(x for x in range(N) if x not in A)
         sig = list(itertools.permutations(A))
         tau = list(itertools.permutations(Ac))
@@ -272,8 +343,12 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
                 lam = {x: (hi >> pos[x]) & 1 for x in A}
                 hpar = (hi & 1) | sum(lam[sg[l]] << (l + 1) for l in range(j - 1))
                 parent = lay["U"] + (hi & 1) * SP if j == 1 else in_off(sg[:-1], hpar, local_in)
-                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)),
-                            leaf_off(lay["PHI"], n_hi, si, hi)))
+                if mma:
+                    sl = mma_slot(plan.mma_assign[si_], A, hi, MMA_COL_POS)
+                    dst = lay["PHI"] + (si * n_hi + sl) * 8
+                else:
+                    dst = leaf_off(lay["PHI"], n_hi, si, hi)
+                phi.append((parent, eps_off(sg[-1], lam[sg[-1]]), mask_off(mask_of(A)), dst))
         ub = []
         L = N - j
         for ti, tu in enumerate(tau):
@@ -281,7 +356,15 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
                 lam = {x: (ho >> pos[x]) & 1 for x in Ac}
                 hpar = (ho & 1) | sum(lam[tu[l]] << (l + 1) for l in range(L - 1))
                 parent = lay["UB"] + (ho & 1) * SP if L == 1 else out_off(tu[:-1], hpar, local_out)
-                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, leaf_off(lay["UBL"], n_ho, ti, ho)))
+                if mma:
+                    sl = mma_slot(plan.mma_assign[si_], Ac, ho, MMA_ROW_POS)
+                    dst = lay["UBL"] + (ti * n_ho + sl) * 8
+                else:
+                    dst = leaf_off(lay["UBL"], n_ho, ti, ho)
+                ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, dst))
+        if mma:   # consecutive lanes store consecutive AoS spinors (conflict-free with the XOR swizzle)
+            phi.sort(key=lambda t: t[3])
+            ub.sort(key=lambda t: t[3])
         stages.append([("phi", phi), ("ub", ub)])
         plan.set_stages.append(stages)
 
