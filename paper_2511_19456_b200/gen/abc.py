@@ -39,7 +39,7 @@ def _subset_prelude(N, L):
     """Q_S and r(S) for every proper non-empty subset, by increasing size (Q_S = Q_{S minus max} + q_max).
     For N >= BATCH_INV_MIN_N the reciprocals of one size are taken together (Montgomery's batch inversion:
     prefix products, one division, two multiplications back per subset), so a subset costs 3
-    multiplications instead of an FP64 division (a reciprocal-estimate + Newton sequence, ~8 FP64 pipe
+    multiplications and a Newton step (2 FMA) instead of an FP64 division (a reciprocal-estimate + Newton sequence, ~8 FP64 pipe
     operations); the chains of the N - 1 sizes are independent."""
     if N < BATCH_INV_MIN_N:
         return _subset_prelude_div(N, L)
@@ -63,10 +63,14 @@ def _subset_prelude(N, L):
             L.append(f"  const double pp{size}_{i} = pp{size}_{i - 1} * d{names[i]};")
         L.append(f"  double iv{size} = 1.0 / pp{size}_{len(names) - 1};")
         for i in range(len(names) - 1, 0, -1):
-            L.append(f"  const double r{names[i]} = iv{size} * pp{size}_{i - 1};")
+            L.append(f"  const double q{names[i]} = iv{size} * pp{size}_{i - 1};")
             L.append(f"  iv{size} *= d{names[i]};")
-        L.append(f"  const double r{names[0]} = iv{size};")
-        flops += 3 * (len(names) - 1) + 1
+        L.append(f"  const double q{names[0]} = iv{size};")
+        # one Newton step per reciprocal: the chain's error grows with its length (and the diagram sum can
+        # cancel by 1e5, tests/test_abc_gpu.py full-size case); r = q + q (1 - d q) is back to ~1 ulp
+        for nm in names:
+            L.append(f"  const double r{nm} = fma(q{nm}, fma(-d{nm}, q{nm}, 1.0), q{nm});")
+        flops += 3 * (len(names) - 1) + 1 + 4 * len(names)
     return flops
 
 

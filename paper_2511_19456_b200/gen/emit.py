@@ -236,8 +236,8 @@ def plan_variants(N: int) -> list[Plan]:
         plans.append(make_plan(N, mma=True))
     if N == 5:
         plans.append(make_plan(N, store=1))
-        # tensor-core joins with less shared memory per point (more resident points): sweep r56
-        plans += [make_plan(N, mma=True, store=1), make_plan(N, mma=True, store=1, sp=8), make_plan(N, mma=True, sp=8)]
+        # (r56: tensor-core joins with less shared memory per point -- level 2 recomputed per subset, or the
+        # 64-byte interior pitch -- measured 15-24 % slower than the default tensor-core plan: dropped)
         # (r38: the 64-byte spinor pitch, 22 KB per point and 10 resident points per SM, measured 11-16 % slower)
     return plans
 
