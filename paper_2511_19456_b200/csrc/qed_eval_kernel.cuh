@@ -143,12 +143,16 @@ struct BGTasks {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
     double m[5];
     ld_mask(b + d[0], m);
-    st_leaf<T::NHI>(b + d[1], prop_col(m, vsum<K, false>(b, raw)));
+    const spinor v = prop_col(m, vsum<K, false>(b, raw));
+    if constexpr (mma_of<T>::value) st_aos<8>(b, d[1], v);   // tensor-core joins: AoS leaves
+    else st_leaf<T::NHI>(b + d[1], v);
   }
   template <int K>
   static __device__ __forceinline__ void out_leaf(double* b, const D& raw) {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(&raw);
-    st_leaf<T::NHO>(b + d[1], vsum<K, true>(b, raw));
+    const spinor v = vsum<K, true>(b, raw);
+    if constexpr (mma_of<T>::value) st_aos<8>(b, d[1], v);
+    else st_leaf<T::NHO>(b + d[1], v);
   }
 };
 
@@ -780,25 +784,34 @@ __device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int 
     for (int tr = 0; tr < TR; ++tr)
 #pragma unroll
       for (int tc = 0; tc < TC; ++tc) acc[p][tr][tc] = MmaAcc{{0.0, 0.0}, {0.0, 0.0}};
+  // a 64-lane group: its two warps take half of the sigma rows (CDAG) or every other subset (Berends-Giele,
+  // one sigma row); both apply every accumulator exchange
   const int half = T::G > 32 ? (threadIdx.x >> 5) & 1 : 0;
-  const int sg0 = T::G > 32 ? half * (T::NSIG / 2) : 0, sg1 = T::G > 32 ? sg0 + T::NSIG / 2 + (half ? T::NSIG % 2 : 0) : T::NSIG;
+  constexpr bool SPLIT_SIG = T::G > 32 && T::NSIG > 1, SPLIT_SET = T::G > 32 && T::NSIG == 1;
+  const int sg0 = SPLIT_SIG ? half * (T::NSIG / 2) : 0, sg1 = SPLIT_SIG ? sg0 + T::NSIG / 2 + (half ? T::NSIG % 2 : 0) : T::NSIG;
   typename sd_of<T, DP != 0>::type sd;
   if constexpr (DP) T::load_set(sd, g, 0);
 #pragma unroll 1
-  for (int si = 0; si < T::NSETS; ++si) {
+  for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {   // leaf stage of SETB subsets (CDAG: one)
     if constexpr (DP) {
       T::run_set_d(base, g, pb, sd);
       group_sync<T>(pb);
-      if (si + 1 < T::NSETS) T::load_set(sd, g, si + 1);
+      if (s0 + T::SETB < T::NSETS) T::load_set(sd, g, s0 + T::SETB);
     } else {
-      T::run_set(base, g, pb, si);
+      T::run_set(base, g, pb, s0);
       group_sync<T>(pb);
     }
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const double* pbase = T::G > 32 ? base : smem + (w * P + p) * T::STRIDE;
-      join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
-      if (si + 1 < T::NSETS) T::mma_swap(acc[p], lane, si);
+    for (int lb = 0; lb < T::SETB; ++lb) {
+      const int si = s0 + lb;
+      if (T::NSETS_REAL % T::SETB == 0 || si < T::NSETS_REAL) {   // padding subsets: leaves only
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const double* pbase = (T::G > 32 ? base : smem + (w * P + p) * T::STRIDE) + lb * T::LEAFB;
+          if (!SPLIT_SET || (si & 1) == half) join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
+          if (si + 1 < T::NSETS_REAL) T::mma_swap(acc[p], lane, si);
+        }
+      }
     }
     group_sync<T>(pb);
   }

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import os
 
-from .emit import choose_launch, lane_offset
+from .emit import _mma_members, choose_launch, lane_offset
 from .lower import hiho_table, hs_table
 import math
 
@@ -162,7 +162,7 @@ struct T {{
   static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = {plan.n_sets_real}, SETB = {B}, LEAFB = {L['LEAFB']};
   static constexpr int HS = {plan.hs}, NAMP = 4 * HS;   // join halves, amplitudes per lane
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
-  static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
+{_mma_members(plan) if getattr(plan, "mma", False) else ""}  static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
   static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
   static __device__ __forceinline__ uint2 hs_offsets(int si, int gh) {{ return __ldg(k_hs + si * (G / 2) + gh); }}
@@ -205,10 +205,13 @@ def emit_bg_source(plan: BGPlan, extras: tuple = ()) -> str:
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{k}, true>\n"
         f"                                      : (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{k}, false>;"
         for i, (ns, k, _, _) in enumerate(allv))
-    mcases = "\n".join(f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{ns}::T, {ns}::V{k}>;"
-                       for i, (ns, k, _, _) in enumerate(allv))
     n = len(allv)
-    mcv = 1 if (N in PROMOTE and extras) else 0      # the original default plan's V0
+    # the fused MC kernel runs the CUDA-core joins of the original default plan (its V0)
+    mcv = next(i for i, (ns, k, _, p) in enumerate(allv) if ns == f"qedbg_N{N}" and k == 0)
+    mns, mk = allv[mcv][0], allv[mcv][1]
+    mcases = "\n".join(f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<"
+                       f"{mns if getattr(p, 'mma', False) else ns}::T, {mns if getattr(p, 'mma', False) else ns}::V{mk if getattr(p, 'mma', False) else k}>;"
+                       for i, (ns, k, _, p) in enumerate(allv))
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_bg.py -- do not edit.
 // Berends-Giele (distributive rewrite of the node-reduced CDAG, NEXT #1) for N = {N} photons (n = {N - 1}):
 // {plan.n_sets_real} photon subsets A (|A| = j = {plan.j}), one join each, {plan.H} configurations per point.
@@ -253,18 +256,21 @@ void qedbg_config_N{N}(int variant, int* warps_per_block, int* points_per_warp, 
 # the wider tasks leave more lanes idle in each divergent in-/out-leaf phase, lower_bg.simt_utilisation);
 # ungrouped candidates with the subset batch the SIMT model prefers (sweep r52)
 CANDIDATES = {
-    5: [dict(setb=4), dict(setb=3)],
+    4: [dict(mma=True)],
+    5: [dict(setb=4), dict(setb=3), dict(mma=True, setb=4)],
     6: [dict(grp=(1, 2, 1, 1, 1), setb=4), dict(setb=4), dict(setb=6)],
     7: [dict(setb=5, hs=1)],
 }
 
 
 # (candidate, its variant) promoted to variant 0 where the sweep measured it faster than the default plan
-# (profiles/sweep_r52_setb.jsonl, B200 at 1965 MHz): n = 4 SETB 4 + descriptor prefetch +3.2 %, n = 5 SETB 4
-# (12 blocks/SM) +8.7 %, n = 6 SETB 5 with one-tile joins +7.2 %; n = 7, 8 candidates (SETB 3, 4, one-tile
-# joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl) and were dropped.  The fused MC kernel keeps
-# the original default plan (qedbg_mc_variant_N*: the promoted n = 4 plan measured 3.7 % slower inside MC)
-PROMOTE = {5: (0, 2), 6: (1, 1), 7: (0, 0)}
+# (B200 at 1965 MHz): n = 5 SETB 4 at 12 blocks/SM +8.7 %, n = 6 SETB 5 with one-tile joins +7.2 %
+# (profiles/sweep_r52_setb.jsonl); tensor-core joins (make_bg_plan(mma=True), profiles/sweep_r58_bg_mma.jsonl)
+# n = 3 +4.9 %, n = 4 +3.8 % over the previous defaults -- at n = 5 the accumulator exchanges (one per subset,
+# against only one (sigma, tau) join each) cost more than the joins save: -16 %, not kept; n = 7, 8 candidates
+# (SETB 3, 4, one-tile joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl).  The fused MC kernel
+# keeps the original default plan (qedbg_mc_variant_N*: the SETB 4 n = 4 plan measured 3.7 % slower inside MC)
+PROMOTE = {4: (0, 2), 5: (2, 2), 6: (1, 1), 7: (0, 0)}
 
 
 def candidate_plans(N: int) -> list[dict]:

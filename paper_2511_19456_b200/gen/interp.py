@@ -71,6 +71,36 @@ def _join_offsets_hs(tab, plan, si, h):
 MMA_BIT = {"L0": ("col", 1), "L1": ("col", 2), "TC": ("col", 3), "L3": ("row", 1), "L4": ("row", 2), "TR": ("row", 3)}
 
 
+def _mma_swap(acc, swap):
+    """Exchange of the two accumulator bits of one subset transition (qed_eval_kernel.cuh mma_swap_*)."""
+    pa, pc = swap
+    (_, ba), (_, bc) = MMA_BIT[pa], MMA_BIT[pc]
+    R, C = acc.shape
+    new = np.empty_like(acc)
+    for r in range(R):
+        for c in range(C):
+            r2 = (r & ~(1 << bc)) | (((c >> ba) & 1) << bc)
+            c2 = (c & ~(1 << ba)) | (((r >> bc) & 1) << ba)
+            new[r][c] = acc[r2][c2]
+    return new
+
+
+def _mma_amp(plan, acc):
+    """Accumulator (row, col) -> amplitude of its configuration under the last subset's assignment."""
+    N = plan.N
+    R, C = acc.shape
+    assign = plan.mma_assign[-1] if not hasattr(plan, "n_sets_real") else plan.mma_assign[plan.n_sets_real - 1]
+    amp = np.zeros(plan.H, dtype=complex)
+    for r in range(R):
+        for c in range(C):
+            h = (c & 1) | ((r & 1) << (N + 1))
+            for x, pos in assign.items():
+                side, b = MMA_BIT[pos]
+                h |= (((c if side == "col" else r) >> b) & 1) << (1 + x)
+            amp[h] = acc[r][c]
+    return amp
+
+
 def _mma_join(plan, sm, run, get_aos_sp8):
     """The tensor-core join of qed_eval_kernel.cuh (join_mma) on one point: per subset (Johnson order),
     C[row][col] += sum_c ubar_tau[row][c] phi_sigma[col][c] over every diagram (sigma, tau), with rows / cols
@@ -251,6 +281,11 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
     LB = L["LEAFB"]
 
     def put_leaf(nh, off, v):     # off: the descriptor's leaf offset (component 0)
+        if getattr(plan, "mma", False):   # AoS leaves, 64-byte pitch with the XOR swizzle
+            for c in range(4):
+                o = aos_slot(off, c, 8)
+                sm[o], sm[o + 1] = v[c].real, v[c].imag
+            return
         for c in range(4):
             o = off + c * nh * 2
             sm[o], sm[o + 1] = v[c].real, v[c].imag
@@ -327,6 +362,19 @@ def eval_point_bg(plan, mom: np.ndarray, n_in_ph: int) -> np.ndarray:
                 for d in nodes(plan.set_out[sj], N - plan.j, plan.f_out, True):
                     put_leaf(plan.n_ho, d[1], vsum(d, True))
         if si >= plan.n_sets_real:      # padding subset of a ragged last batch
+            continue
+        if getattr(plan, "mma", False):
+            R, C = plan.n_ho, plan.n_hi
+
+            def aos8(off):
+                return np.array([complex(sm[aos_slot(off, c, 8)], sm[aos_slot(off, c, 8) + 1]) for c in range(4)])
+            U = np.array([aos8(L["UBL"] + lb * LB + r * 8) for r in range(R)])
+            P = np.array([aos8(L["PHI"] + lb * LB + c * 8) for c in range(C)])
+            mma_acc = (mma_acc if si else np.zeros((R, C), dtype=complex)) + U @ P.T
+            if si + 1 < plan.n_sets_real:
+                mma_acc = _mma_swap(mma_acc, plan.mma_swaps[si])
+            if si + 1 == plan.n_sets_real:
+                amp[:] = _mma_amp(plan, mma_acc)
             continue
         for h in range(H):
             if hst is not None:

@@ -26,7 +26,7 @@ import math
 from dataclasses import dataclass, field
 
 from .dag import balanced_split
-from .lower import FLOPS, PITCH_BG, lane_offset, leaf_off
+from .lower import FLOPS, MMA_COL_POS, MMA_ROW_POS, PITCH_BG, johnson_order, lane_offset, leaf_off, mma_assignments
 
 FLOPS_BG = dict(FLOPS)
 FLOPS_BG["VACC"] = 48    # accumulating vertex: 8 real outputs x 3 fma
@@ -260,8 +260,17 @@ def task_flops(K: int, F: int, prop: bool) -> int:
     return tot
 
 
+def mma_leaf_slot(assign: dict, side_photons, h: int, prim) -> int:
+    """Accumulator-layout slot of leaf helicity h (bit 0 = s / s', bit 1 + k = lam of the k-th sorted photon
+    of the side): bit 0 <- the spin, bits 1, 2, 3 <- the photons at prim[0], prim[1], prim[2] (lower.py)."""
+    slot = h & 1
+    for k, x in enumerate(side_photons):
+        slot |= ((h >> (1 + k)) & 1) << (1 + prim.index(assign[x]))
+    return slot
+
+
 def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: int | None = None,
-                 sp: int | None = None, hs: int | None = None, grp: tuple | None = None) -> BGPlan:
+                 sp: int | None = None, hs: int | None = None, grp: tuple | None = None, mma: bool = False) -> BGPlan:
     if j is None:
         j = balanced_split(N)
     assert 1 <= j <= N - 1
@@ -270,6 +279,9 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     SP = sp if sp is not None else PITCH_BG.get(N, 10)
     grp = tuple(grp) if grp is not None else (0, 0, 0, 0, 0)
     grouped = any(grp)
+    if mma:   # tensor-core joins (qed_eval_kernel.cuh mma_eval): one-tile joins, ungrouped tasks
+        assert not grouped and (hs in (None, 1)) and j <= len(MMA_COL_POS) and N - j <= len(MMA_ROW_POS)
+        hs = 1
     if store is None:
         store = default_bg_store(N, j)
     assert not grouped or store + 1 >= max(j, N - j), "grouped plans store every interior level"
@@ -312,7 +324,7 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     set_local: dict[tuple, int] = {}
     cur_slot = [0]
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
-    leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL)
+    leafb = (4 * n_hi * 2 + 4 * n_ho * 2 + 7) // 8 * 8      # doubles per leaf buffer (PHI + UBL; AoS if mma)
     if grouped:   # leaf buffers of one batch skewed by the out-leaf tasks per subset (16-byte columns): the
         # quarter warps storing the same columns of several subsets hit distinct bank groups
         leafb += (2 << max(0, N - j - min(grp[3], N - j) + 1)) % 16
@@ -431,7 +443,10 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         if k < N - j:
             t = level_tasks("out", _subsets(N, k), "lvl")
             plan.levels.append(("out", k, t, fsel("lvl", k)))
-    subsets = list(itertools.combinations(range(N), j))
+    subsets = johnson_order(N, j) if mma else list(itertools.combinations(range(N), j))
+    plan.mma = mma
+    if mma:
+        plan.mma_assign, plan.mma_swaps = mma_assignments(N, j, subsets)
     if hs == 2:
         # two-half joins (lower.hs_table): subsets containing photon N-1 first, so that the two halves
         # of a batch take the same join shape (at most one mixed pair)
@@ -469,8 +484,18 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
         plan.set_stages.append(stages)
         lb = (len(plan.sets) - 1) % setb          # leaf buffer of this subset within its batch
         phi0, ubl0 = lay["PHI"] + lb * lay["LEAFB"], lay["UBL"] + lb * lay["LEAFB"]
-        plan.set_in.append(level_tasks("in", [A], "in_leaf", phi0, n_hi))
-        plan.set_out.append(level_tasks("out", [Ac], "out_leaf", ubl0, n_ho))
+        if mma:   # AoS leaves at their accumulator-layout slot (lower.mma_slot), tasks in slot order
+            si_ = min(len(plan.sets) - 1, plan.n_sets_real - 1)
+            asg = plan.mma_assign[si_]
+            ti = [(d, mma_leaf_slot(asg, A, d_h, MMA_COL_POS)) for d, d_h in
+                  zip(level_tasks("in", [A], "in_leaf", phi0, n_hi), range(n_hi))]
+            plan.set_in.append(sorted(([d[0], phi0 + sl * 8] + d[2:] for d, sl in ti), key=lambda t: t[1]))
+            to = [(d, mma_leaf_slot(asg, Ac, d_h, MMA_ROW_POS)) for d, d_h in
+                  zip(level_tasks("out", [Ac], "out_leaf", ubl0, n_ho), range(n_ho))]
+            plan.set_out.append(sorted(([d[0], ubl0 + sl * 8] + d[2:] for d, sl in to), key=lambda t: t[1]))
+        else:
+            plan.set_in.append(level_tasks("in", [A], "in_leaf", phi0, n_hi))
+            plan.set_out.append(level_tasks("out", [Ac], "out_leaf", ubl0, n_ho))
 
     F = FLOPS_BG
     H = 1 << (N + 2)
