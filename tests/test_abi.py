@@ -66,3 +66,12 @@ def test_errors_without_gpu_are_reported_not_raised():
         assert e.status == 3
     else:
         raise AssertionError("expected QED_ERR_CUDA without a GPU")
+
+
+def test_tensor_core_joins_are_compiled():
+    """The default n = 3..5 CDAG kernels join on the FP64 tensor core: the library's SASS holds DMMA
+    instructions (DESIGN.md kernel 2-MMA), and the CUDA-core FP64 path (DFMA) beside them."""
+    import subprocess
+    from paper_2511_19456_b200 import qed
+    sass = subprocess.run(["cuobjdump", "-sass", qed.LIB_PATH], capture_output=True, text=True).stdout
+    assert "DMMA.8x8x4" in sass and "DFMA" in sass

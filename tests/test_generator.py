@@ -302,3 +302,53 @@ def test_bg_grouped_layout_claims_fail_on_a_wrong_stride():
     finally:
         interp.expand_group = orig
     assert np.max(np.abs(A[0] - B)) > 1e-6 * np.max(np.abs(A[0]))
+
+
+# ---------------------------------------------------------------- tensor-core joins (DMMA; this round)
+def test_johnson_order_exchanges_one_photon_per_step():
+    """The subset order of the tensor-core plans visits every j-subset once and consecutive subsets
+    exchange exactly one photon, so the accumulator layout changes by one bit exchange (mma_swap)."""
+    import itertools
+    from paper_2511_19456_b200.gen.lower import johnson_order, mma_assignments
+    for N, j in [(4, 2), (5, 2), (6, 3), (7, 3)]:
+        order = johnson_order(N, j)
+        assert sorted(order) == list(itertools.combinations(range(N), j))
+        for a, b in zip(order, order[1:]):
+            assert len(set(a) & set(b)) == j - 1
+        if N - j <= 3:
+            assign, swaps = mma_assignments(N, j, order)
+            assert len(swaps) == len(order) - 1
+            for A, asg in zip(order, assign):   # A's photons on column positions, the rest on row positions
+                assert all(asg[x] in ("L0", "L1", "TC") for x in A)
+                assert all(asg[x] in ("L3", "L4", "TR") for x in range(N) if x not in A)
+                assert len(set(asg.values())) == N
+
+
+@pytest.mark.parametrize("N,bg", [(4, False), (5, False), (6, False), (4, True), (5, True), (6, True)])
+def test_mma_plans_interpreted_match_oracle(N, bg):
+    """Tensor-core-join plans (AoS leaves at their accumulator slot, Johnson order, per-subset bit exchanges,
+    final configuration map), executed by the interpreter with the kernel's rules, give the oracle's
+    amplitudes (CDAG: gen/lower.py make_plan(mma=True); Berends-Giele: make_bg_plan(mma=True))."""
+    from paper_2511_19456_b200.gen.interp import eval_point, eval_point_bg
+    from paper_2511_19456_b200.gen.lower import make_plan
+    from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
+    n = N - 1
+    plan = make_bg_plan(N, mma=True) if bg else make_plan(N, mma=True)
+    mom = synthetic.rambo_cm(n, 2, sqrt_s=5.0, seed=1000 + n).numpy()
+    A = oracle.amps(1, n, mom)
+    for k in range(2):
+        B = (eval_point_bg if bg else eval_point)(plan, mom[k], 1)
+        assert np.max(np.abs(A[k] - B)) <= 1e-12 * np.max(np.abs(A[k]))
+
+
+def test_mma_wrong_exchange_is_detected():
+    """Self-check: skipping one accumulator bit exchange (or exchanging the wrong pair) scrambles the
+    amplitudes, so the interpreter parity above can fail on a generator / kernel mismatch."""
+    from paper_2511_19456_b200.gen import interp
+    from paper_2511_19456_b200.gen.lower import make_plan
+    plan = make_plan(5, mma=True)
+    mom = synthetic.rambo_cm(4, 1, sqrt_s=5.0, seed=1001).numpy()
+    A = oracle.amps(1, 4, mom)
+    plan.mma_swaps = [plan.mma_swaps[0]] * len(plan.mma_swaps)
+    B = interp.eval_point(plan, mom[0], 1)
+    assert np.max(np.abs(A[0] - B)) > 1e-6 * np.max(np.abs(A[0]))
