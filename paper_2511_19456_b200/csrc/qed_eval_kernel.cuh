@@ -12,6 +12,8 @@
 //
 // Algorithmic work per point: gen/lower.py Plan.flops.
 #pragma once
+#include <utility>
+
 #include "qed_device.cuh"
 #include "qed_kernel_args.h"
 
@@ -622,6 +624,17 @@ struct dp_of<V, decltype(void(V::DP))> {
   static constexpr int value = V::DP;
 };
 
+// launch-variant field UR (tensor-core plans): the subset loop fully unrolled, so every accumulator exchange
+// is straight-line code (no switch on the subset index); variants without the field read 0
+template <class V, class = void>
+struct ur_of {
+  static constexpr int value = 0;
+};
+template <class V>
+struct ur_of<V, decltype(void(V::UR))> {
+  static constexpr int value = V::UR;
+};
+
 struct NoSD {};
 template <class T, bool HAS>
 struct sd_of {
@@ -765,6 +778,42 @@ __device__ __forceinline__ double group_msq(const double (&amp)[2 * T::NAMP], in
   return a.norm * sum;
 }
 
+// the subset loop of mma_eval unrolled (launch field UR): batch B is a compile-time constant, so
+// T::mma_swap(acc, lane, si) folds to the one exchange of that subset
+template <class T, int DP, int P, int B, class SD>
+__device__ __forceinline__ void mma_batch(double* smem, double* base, int g, int pb, int w, int lane, int half, int sg0, int sg1,
+                                          SD& sd, MmaAcc (&acc)[P][Mma<T>::TR][Mma<T>::TC]) {
+  constexpr int s0 = B * T::SETB;
+  constexpr bool SPLIT_SET = T::G > 32 && T::NSIG == 1;
+  if constexpr (DP) {
+    T::run_set_d(base, g, pb, sd);
+    group_sync<T>(pb);
+    if constexpr (s0 + T::SETB < T::NSETS) T::load_set(sd, g, s0 + T::SETB);
+  } else {
+    T::run_set(base, g, pb, s0);
+    group_sync<T>(pb);
+  }
+#pragma unroll
+  for (int lb = 0; lb < T::SETB; ++lb) {
+    const int si = s0 + lb;
+    if (si < T::NSETS_REAL) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double* pbase = (T::G > 32 ? base : smem + (w * P + p) * T::STRIDE) + lb * T::LEAFB;
+        if (!SPLIT_SET || (si & 1) == half) join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
+        if (si + 1 < T::NSETS_REAL) T::mma_swap(acc[p], lane, si);
+      }
+    }
+  }
+  group_sync<T>(pb);
+}
+template <class T, int DP, int P, class SD, int... Bs>
+__device__ __forceinline__ void mma_subsets(double* smem, double* base, int g, int pb, int w, int lane, int half, int sg0,
+                                            int sg1, SD& sd, MmaAcc (&acc)[P][Mma<T>::TR][Mma<T>::TC],
+                                            std::integer_sequence<int, Bs...>) {
+  (mma_batch<T, DP, P, Bs>(smem, base, g, pb, w, lane, half, sg0, sg1, sd, acc), ...);
+}
+
 // Stages 1-4 of a tensor-core-join plan for the points of this warp (after stage 0).  Groups of G <= 32 lanes
 // run their own point's tasks; the joins are warp-wide, one point after the other (P per warp).  A 64-lane
 // group splits the sigma rows between its two warps and sums the halves through shared memory.
@@ -791,6 +840,9 @@ __device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int 
   const int sg0 = SPLIT_SIG ? half * (T::NSIG / 2) : 0, sg1 = SPLIT_SIG ? sg0 + T::NSIG / 2 + (half ? T::NSIG % 2 : 0) : T::NSIG;
   typename sd_of<T, DP != 0>::type sd;
   if constexpr (DP) T::load_set(sd, g, 0);
+  if constexpr (ur_of<V>::value) {
+    mma_subsets<T, DP, P>(smem, base, g, pb, w, lane, half, sg0, sg1, sd, acc, std::make_integer_sequence<int, T::NSETS / T::SETB>{});
+  } else {
 #pragma unroll 1
   for (int s0 = 0; s0 < T::NSETS; s0 += T::SETB) {   // leaf stage of SETB subsets (CDAG: one)
     if constexpr (DP) {
@@ -814,6 +866,7 @@ __device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int 
       }
     }
     group_sync<T>(pb);
+  }
   }
   if constexpr (T::G > 32) {   // second warp's partial tiles -> the (dead) leaf rows of the point, summed by the first
     double* red = base + T::PHI;

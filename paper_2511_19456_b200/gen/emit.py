@@ -224,7 +224,8 @@ struct T {{
 # tensor-core-join variant promoted to variant 0 (index among the mma variants), where measured faster
 # (profiles/sweep_r55_mma.jsonl: n = 3 +17 %, n = 4 +19 %, n = 5 +24 % over the CUDA-core join, with the
 # descriptor prefetch)
-MMA_PROMOTE: dict[int, int] = {4: 0, 5: 0, 6: 0}
+# + (r60) the unrolled subset loop at n = 3
+MMA_PROMOTE: dict[int, int] = {4: 3, 5: 0, 6: 0}
 
 
 def plan_variants(N: int) -> list[Plan]:
@@ -251,6 +252,8 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
         if getattr(p, "mma", False):   # tensor-core joins: no accumulator split / sigma blocking; +- descriptor prefetch
             wpb, mb = choose_launch(p)
             vs += [(pi, wpb, mb, 2, 2, 1, 1), (pi, wpb, mb, 2, 2, 1, 0)]
+            if N <= 5:   # unrolled subset loop (UR); r60: n = 3 +5.6 %, n = 4 +0.8 %, n = 5 -28 % (20 subsets: code size)
+                vs += [(pi, wpb, mb, 2, 2, 1, 1, 1), (pi, wpb, mb, 2, 2, 1, 0, 1)]
         else:
             vs += [(pi,) + v for v in variants(p)]
     mma_v = [i for i, v in enumerate(vs) if getattr(plans[v[0]], "mma", False)]
@@ -262,8 +265,9 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     bodies = "\n".join(emit_plan_namespace(p, ns) for p, ns in zip(plans, nss))
     variant_structs = "".join(
-        f"namespace {nss[pi]} {{ struct V{i} {{ static constexpr int WPB = {w}, MIN_BLOCKS = {m}, AS = {a}, PF = {p}, SB = {sb}, DP = {dp}; }}; }}\n"
-        for i, (pi, w, m, a, p, sb, dp) in enumerate(vs))
+        f"namespace {nss[v[0]]} {{ struct V{i} {{ static constexpr int WPB = {v[1]}, MIN_BLOCKS = {v[2]}, AS = {v[3]}, PF = {v[4]}, "
+        f"SB = {v[5]}, DP = {v[6]}{f', UR = {v[7]}' if len(v) > 7 else ''}; }}; }}\n"
+        for i, v in enumerate(vs))
     kernel_cases = "\n".join(
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, false>;"
