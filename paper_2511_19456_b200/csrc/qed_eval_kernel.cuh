@@ -577,31 +577,24 @@ __device__ __forceinline__ void mma_swap_ll(MmaAcc (&acc)[TR][TC], int lane) {
         acc[tr][tc].im[r] = __shfl_sync(0xffffffffu, acc[tr][tc].im[r], src);
       }
 }
-// lane bit A <-> tile index bit (ROW: the row tile TR, else the column tile TC)
+// lane bit A <-> tile index bit (ROW: the row tile TR, else the column tile TC).  Element (lane L, tile t) takes
+// the element of tile bit(L, A) from the lane whose bit A is t: a lane keeps tile bit(L, A) and swaps the other
+// tile with its partner L ^ (1 << A) -- one shuffle per pair of tiles
 template <int A, bool ROW, int TR, int TC>
 __device__ __forceinline__ void mma_swap_lt(MmaAcc (&acc)[TR][TC], int lane) {
-  const int la = (lane >> A) & 1;
-  MmaAcc o[TR][TC];
+  const bool la = (lane >> A) & 1;
 #pragma unroll
-  for (int tr = 0; tr < TR; ++tr)
+  for (int o = 0; o < (ROW ? TC : TR); ++o) {
+    MmaAcc& t0 = ROW ? acc[0][o] : acc[o][0];
+    MmaAcc& t1 = ROW ? acc[TR - 1][o] : acc[o][TC - 1];
 #pragma unroll
-    for (int tc = 0; tc < TC; ++tc) o[tr][tc] = acc[tr][tc];
-#pragma unroll
-  for (int tr = 0; tr < TR; ++tr)
-#pragma unroll
-    for (int tc = 0; tc < TC; ++tc) {
-      const int t = ROW ? tr : tc;            // the new element's tile bit = the source lane's bit A
-      const int src = (lane & ~(1 << A)) | (t << A);
-      const MmaAcc& s0 = ROW ? o[0][tc] : o[tr][0];
-      const MmaAcc& s1 = ROW ? o[TR - 1][tc] : o[tr][TC - 1];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const double x0 = __shfl_sync(0xffffffffu, s0.re[r], src), x1 = __shfl_sync(0xffffffffu, s1.re[r], src);
-        const double y0 = __shfl_sync(0xffffffffu, s0.im[r], src), y1 = __shfl_sync(0xffffffffu, s1.im[r], src);
-        acc[tr][tc].re[r] = la ? x1 : x0;
-        acc[tr][tc].im[r] = la ? y1 : y0;
-      }
+    for (int r = 0; r < 2; ++r) {
+      const double sre = la ? t0.re[r] : t1.re[r], sim = la ? t0.im[r] : t1.im[r];   // the tile the partner needs
+      const double zre = __shfl_xor_sync(0xffffffffu, sre, 1 << A), zim = __shfl_xor_sync(0xffffffffu, sim, 1 << A);
+      if (la) { t0.re[r] = zre; t0.im[r] = zim; }
+      else { t1.re[r] = zre; t1.im[r] = zim; }
     }
+  }
 }
 // column tile <-> row tile
 template <int TR, int TC>

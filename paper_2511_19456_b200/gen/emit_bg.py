@@ -267,7 +267,8 @@ CANDIDATES = {
 # (B200 at 1965 MHz): n = 5 SETB 4 at 12 blocks/SM +8.7 %, n = 6 SETB 5 with one-tile joins +7.2 %
 # (profiles/sweep_r52_setb.jsonl); tensor-core joins (make_bg_plan(mma=True), profiles/sweep_r58_bg_mma.jsonl)
 # n = 3 +4.9 %, n = 4 +3.8 % over the previous defaults -- at n = 5 the accumulator exchanges (one per subset,
-# against only one (sigma, tau) join each) cost more than the joins save: -16 %, not kept; n = 7, 8 candidates
+# against only one (sigma, tau) join each) cost more than the joins save: -16 %, -9 % with the one-shuffle
+# lane-tile exchange (r62), not kept; n = 7, 8 candidates
 # (SETB 3, 4, one-tile joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl).  The fused MC kernel
 # keeps the original default plan (qedbg_mc_variant_N*: the SETB 4 n = 4 plan measured 3.7 % slower inside MC)
 PROMOTE = {4: (0, 2), 5: (2, 2), 6: (1, 1), 7: (0, 0)}
