@@ -85,7 +85,8 @@ qed_status qed_process_create(const qed_state_spec* in, const qed_state_spec* ou
    at n = 2 both run one-thread-per-point register kernels, at n >= 3 lane-group kernels.
    variant: launch-variant index (tuning), -1 = default / QED_VARIANT environment variable; an index
    >= qed_process_info.n_variants, or a QED_VARIANT that is not such an index, is
-   QED_ERR_INVALID_ARGUMENT (no silent fallback).
+   QED_ERR_INVALID_ARGUMENT (no silent fallback).  With the default, qed_eval_msq* and qed_mc_sum each run
+   their own best launch plan; an explicit variant applies to both (lane-group kernels).
    kernel_family: QED_FAMILY_DEFAULT picks the register kernels at n <= 2 and the lane-group kernels
    above; QED_FAMILY_LANE_GROUP forces the lane-group kernels at n <= 2 too (comparison runs).
    No other environment variable changes what the library does. */

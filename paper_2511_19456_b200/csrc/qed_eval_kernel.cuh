@@ -810,8 +810,11 @@ __device__ __forceinline__ void mma_subsets(double* smem, double* base, int g, i
 // Stages 1-4 of a tensor-core-join plan for the points of this warp (after stage 0).  Groups of G <= 32 lanes
 // run their own point's tasks; the joins are warp-wide, one point after the other (P per warp).  A 64-lane
 // group splits the sigma rows between its two warps and sums the halves through shared memory.
-template <class T, class V, bool PER_CONFIG>
-__device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int pb, const QedEvalArgs& a, long long p0) {
+// MODE 0: the averaged |M|^2 to a.out; 1: per configuration to a.out; 2: no store, returns the group's
+// averaged |M|^2 (every lane; the fused MC kernel)
+template <class T, class V, int MODE>
+__device__ __forceinline__ double mma_eval(double* smem, double* base, int g, int pb, const QedEvalArgs& a, long long p0) {
+  constexpr bool PER_CONFIG = MODE == 1;
   constexpr int TR = Mma<T>::TR, TC = Mma<T>::TC, P = Mma<T>::P;
   constexpr int DP = dp_of<V>::value;
   const int lane = threadIdx.x & 31;
@@ -889,6 +892,7 @@ __device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int 
   }
   // stage 4: |amp|^2 per configuration (config of each accumulator element: T::mma_config)
   const long long n = a.n_points;
+  double mine = 0.0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const long long ptp = T::G > 32 ? p0 + pb : p0 + w * P + p;
@@ -922,9 +926,20 @@ __device__ __forceinline__ void mma_eval(double* smem, double* base, int g, int 
           }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (ptp < n && half == 0 && (T::G > 32 ? lane == 0 : lane == p * T::G)) a.out[ptp] = a.norm * sum;
+      if (MODE == 2) {
+        if (T::G > 32 || p == (pb % P)) mine = a.norm * sum;
+      } else if (ptp < n && half == 0 && (T::G > 32 ? lane == 0 : lane == p * T::G)) {
+        a.out[ptp] = a.norm * sum;
+      }
     }
   }
+  if constexpr (MODE == 2 && T::G > 32) {   // the second warp's sum is partial (its acc was added into the first's)
+    group_sync<T>(pb);
+    if (half == 0 && lane == 0) base[T::RED] = mine;
+    group_sync<T>(pb);
+    mine = base[T::RED];
+  }
+  return mine;
 }
 
 // V: launch variant (WPB warps per block, MIN_BLOCKS resident blocks, AS accumulator split, PF prefetch)
@@ -974,7 +989,7 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_eval_kernel(Qe
     }
     group_sync<T>(pb);
     if constexpr (mma_of<T>::value) {
-      mma_eval<T, V, PER_CONFIG>(smem, base, g, pb, a, p0);
+      mma_eval<T, V, PER_CONFIG ? 1 : 0>(smem, base, g, pb, a, p0);
     } else {
     double amp[2 * T::NAMP];
     eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);

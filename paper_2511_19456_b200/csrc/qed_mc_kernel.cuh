@@ -63,75 +63,12 @@ __device__ double rambo_volume(double s) {
   return vol * pow(2.0 * M_PI, 4.0 - 3.0 * K);
 }
 
-// Massive RAMBO for K final particles (particle 0 = electron, m = 1; others massless), steps 2-4, from the
-// massless momenta qin[4 i + mu] (step 1, rambo_massless, one lane per particle), written into mom (particle
-// order e-_in, gamma_in, e-_out, gamma_out...); returns the weight (vol = rambo_volume<K>(s)).
-template <int K>
-__device__ double rambo_point(const double* qin, const QedMcArgs& m, double vol, double* mom) {
-  double q[K][4];
-  double Q[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-#pragma unroll
-    for (int mu = 0; mu < 4; ++mu) {
-      q[i][mu] = qin[4 * i + mu];
-      Q[mu] += q[i][mu];
-    }
-  }
-  const double sqs = m.sqrt_s, s = sqs * sqs;
-  const double M = sqrt(Q[0] * Q[0] - Q[1] * Q[1] - Q[2] * Q[2] - Q[3] * Q[3]);
-  const double b1 = -Q[1] / M, b2 = -Q[2] / M, b3 = -Q[3] / M;
-  const double x = sqs / M, gam = Q[0] / M, aa = 1.0 / (1.0 + gam);
-  double p0[K], pv[K][3];
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const double bq = b1 * q[i][1] + b2 * q[i][2] + b3 * q[i][3];
-    p0[i] = x * (gam * q[i][0] + bq);
-    pv[i][0] = x * (q[i][1] + b1 * q[i][0] + aa * bq * b1);
-    pv[i][1] = x * (q[i][2] + b2 * q[i][0] + aa * bq * b2);
-    pv[i][2] = x * (q[i][3] + b3 * q[i][0] + aa * bq * b3);
-  }
-  // mass rescaling (electron mass 1): Newton on xi from rambo.f's start value
-  double xi = sqrt(1.0 - 1.0 / s);
-  for (int it = 0; it < 50; ++it) {
-    double f = -sqs, df = 0.0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const double mi2 = (i == 0) ? 1.0 : 0.0;
-      const double e = sqrt(mi2 + xi * xi * p0[i] * p0[i]);
-      f += e;
-      df += xi * p0[i] * p0[i] / e;
-    }
-    const double dxi = f / df;
-    xi -= dxi;
-    if (fabs(dxi) <= 1e-15 * xi) break;
-  }
-  // final momenta and weight
-  const double kin = (s - 1.0) / (2.0 * sqs);
-  mom[0] = (s + 1.0) / (2.0 * sqs); mom[1] = 0.0; mom[2] = 0.0; mom[3] = -kin;
-  mom[4] = kin; mom[5] = 0.0; mom[6] = 0.0; mom[7] = kin;
-  double prod = 1.0, sum = 0.0;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const double mi2 = (i == 0) ? 1.0 : 0.0;
-    const double kx = xi * pv[i][0], ky = xi * pv[i][1], kz = xi * pv[i][2];
-    const double E = sqrt(mi2 + xi * xi * p0[i] * p0[i]);
-    const double kk = sqrt(kx * kx + ky * ky + kz * kz);
-    double* o = mom + 8 + 4 * i;
-    o[0] = E; o[1] = kx; o[2] = ky; o[3] = kz;
-    prod *= kk / E;
-    sum += kk * kk / E;
-  }
-  double xp = 1.0;
-#pragma unroll
-  for (int i = 0; i < 2 * K - 3; ++i) xp *= xi;
-  return vol * xp * sqs * prod / sum;
-}
-
-// The same steps 2-4 spread over the lanes of a group (lane i: particle i; every lane of the group's first warp
-// takes part, lanes >= K shadow particle K - 1).  The per-particle square roots and divisions run in parallel;
-// every sum is gathered with shuffles and accumulated in particle order, as in rambo_point, so all lanes hold the
-// same xi and weight and take the same Newton exit.  mom is written by lane i (particle i) and lane 0 (beams).
+// Massive RAMBO steps 2-4 for K final particles (particle 0 = electron, m = 1; others massless) from the massless
+// momenta qin[4 i + mu] (step 1, rambo_massless, one lane per particle), written into mom (particle order e-_in,
+// gamma_in, e-_out, gamma_out...); returns the weight (vol = rambo_volume<K>(s)).
+// The steps are spread over the lanes of a group of G lanes (lane i: particle i; lanes >= K shadow particle K - 1).
+// The per-particle square roots and divisions run in parallel; every sum is gathered with shuffles and accumulated
+// in particle order (as the oracle does), so all lanes hold the same xi and weight and take the same Newton exit.  mom is written by lane i (particle i) and lane 0 (beams).
 template <int K, int G>
 __device__ double rambo_group(const double* qin, const QedMcArgs& m, double vol, double* mom, int g) {
   constexpr int GW = G < 32 ? G : 32;                       // lanes of the group inside this warp
@@ -197,67 +134,80 @@ __device__ double rambo_group(const double* qin, const QedMcArgs& m, double vol,
   return vol * xp * sqs * prod / sum;
 }
 
-// launch-variant field MCS: 1 = RAMBO steps 2-4 serially on lane 0 (round-1 form); absent = 0
-template <class V, class = void>
-struct mcs_of {
-  static constexpr int value = 0;
-};
-template <class V>
-struct mcs_of<V, decltype(void(V::MCS))> {
-  static constexpr int value = V::MCS;
-};
+// RAMBO staging of the fused MC kernel: the block generates RB points per round (one subgroup of SUB >= K lanes
+// per point: 4, 8 or 16; at most 8 eval passes), then evaluates them PB at a time.  Per point: the momenta in the eval slot layout
+// (4 (N + 2) doubles), the weight and the cut flag.  qed_runtime.cu sizes the shared memory with the same rule.
 
 template <class T, class V>
 __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_mc_kernel(QedEvalArgs a, QedMcArgs m) {
   extern __shared__ __align__(16) double smem[];
   constexpr int G = T::G;
-  constexpr int PB = V::WPB * 32 / G;     // points per block
+  constexpr int PB = V::WPB * 32 / G;     // points per block and eval pass (0 if a point spans several warps)
+  constexpr int PBE = PB > 0 ? PB : 1;
   constexpr int K = T::N;                 // final state: electron + n photons = N particles
+  constexpr int SUB = K <= 4 ? 4 : K <= 8 ? 8 : 16;   // RAMBO subgroup: one lane per particle
+  // points per RAMBO round: one per subgroup, at most 8 eval passes (bounds the staging for the 220 KB n = 8 slot)
+  constexpr int RB = V::WPB * 32 / SUB < 8 * PBE ? V::WPB * 32 / SUB : 8 * PBE;
+  constexpr int SD = 4 * (T::N + 2) + 2;
+  static_assert(RB % PBE == 0, "a RAMBO round covers whole eval passes");
   const int g = threadIdx.x % G;
   const int pb = threadIdx.x / G;
   double* base = smem + pb * T::STRIDE;
-  double* red = smem + PB * T::STRIDE;    // [PB][3] block reduction scratch
+  double* red = smem + PBE * T::STRIDE;   // [PB][3] block reduction scratch
+  double* stg = red + 3 * PBE;            // [RB][SD] RAMBO staging
+  const int sg = threadIdx.x / SUB, gl = threadIdx.x % SUB;
   const unsigned long long lo_all = m.first_index, hi_all = m.first_index + m.n_points;
   const unsigned long long c_begin = lo_all / m.chunk, c_end = (hi_all + m.chunk - 1) / m.chunk;
   const double vol = rambo_volume<K>(m.sqrt_s * m.sqrt_s);
-  static_assert(K <= G && 4 * K <= 4 * (T::N + 2), "one lane per particle; q staged in the momentum slot");
   for (unsigned long long c = c_begin + blockIdx.x; c < c_end; c += gridDim.x) {
     const unsigned long long lo = max(lo_all, c * (unsigned long long)m.chunk);
     const unsigned long long hi = min(hi_all, (c + 1) * (unsigned long long)m.chunk);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;  // thread 0 only: fixed summation order over the chunk
-    for (unsigned long long p0 = lo; p0 < hi; p0 += PB) {
-      const unsigned long long idx = p0 + pb;
-      const bool valid = idx < hi;
-      double w = 0.0;
-      bool pass = false;
-      // RAMBO: step 1 one lane per particle; steps 2-4 over the group's first warp (rambo_group; every sum in
-      // particle order, as in the oracle) or, with V::MCS, serially on lane 0 (rambo_point)
-      if (g < K) rambo_massless(valid ? idx : hi - 1, g, m, base + T::MOM + 4 * g);
-      group_sync<T>(pb);
-      if constexpr (mcs_of<V>::value) {
-        if (g == 0) w = rambo_point<K>(base + T::MOM, m, vol, base + T::MOM);
-      } else {
-        // the group's RAMBO lanes are one warp (G <= 32: the group; G = 64: its lanes 0..31)
-        if (g < 32) w = rambo_group<K, G>(base + T::MOM, m, vol, base + T::MOM, g);
-      }
-      group_sync<T>(pb);
-      if (g == 0) {
-        pass = true;
-        for (int i = 1; i < K; ++i) pass = pass && (base[T::MOM + 8 + 4 * i] >= m.omega_min);
-      }
-      double amp[2 * T::NAMP];
-      eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
-      const double msq = group_msq<T>(amp, g, pb, base, a);
-      if (g == 0) {
-        const double v = (valid && pass) ? w * msq : 0.0;
-        red[3 * pb] = v;
-        red[3 * pb + 1] = v * v;
-        red[3 * pb + 2] = (valid && pass) ? 1.0 : 0.0;
+    for (unsigned long long r0 = lo; r0 < hi; r0 += RB) {
+      // RAMBO round: subgroup sg generates point r0 + sg (step 1 one lane per particle, steps 2-4 across the
+      // subgroup: rambo_group; every sum in particle order, as in the oracle)
+      if (sg < RB) {
+        const unsigned long long idx = r0 + sg;
+        double* st = stg + sg * SD;
+        if (gl < K) rambo_massless(idx < hi ? idx : hi - 1, gl, m, st + 8 + 4 * gl);
+        __syncwarp();
+        const double w = rambo_group<K, SUB>(st + 8, m, vol, st, gl);
+        __syncwarp();
+        if (gl == 0) {
+          bool pass = true;
+          for (int i = 1; i < K; ++i) pass = pass && (st[8 + 4 * i] >= m.omega_min);
+          st[SD - 2] = w;
+          st[SD - 1] = pass ? 1.0 : 0.0;
+        }
       }
       __syncthreads();
-      if (threadIdx.x == 0)
-        for (int q = 0; q < PB; ++q) { s0 += red[3 * q]; s1 += red[3 * q + 1]; s2 += red[3 * q + 2]; }
-      __syncthreads();
+      for (int q0 = 0; q0 < RB; q0 += PBE) {
+        const int q = q0 + (PB > 0 ? pb : 0);
+        const unsigned long long idx = r0 + q;
+        const bool valid = idx < hi;
+        const double* st = stg + q * SD;
+        for (int t = g; t < 4 * (T::N + 2); t += G) base[T::MOM + t] = st[t];
+        group_sync<T>(pb);
+        double msq;
+        if constexpr (mma_of<T>::value) {
+          msq = mma_eval<T, V, 2>(smem, base, g, pb, a, 0);
+        } else {
+          double amp[2 * T::NAMP];
+          eval_point<T, V::AS, V::SB, dp_of<V>::value>(base, g, pb, a, amp);
+          msq = group_msq<T>(amp, g, pb, base, a);
+        }
+        if (g == 0) {
+          const bool pass = valid && st[SD - 1] != 0.0;
+          const double v = pass ? st[SD - 2] * msq : 0.0;
+          red[3 * pb] = v;
+          red[3 * pb + 1] = v * v;
+          red[3 * pb + 2] = pass ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+          for (int qq = 0; qq < PBE; ++qq) { s0 += red[3 * qq]; s1 += red[3 * qq + 1]; s2 += red[3 * qq + 2]; }
+        __syncthreads();
+      }
     }
     if (threadIdx.x == 0) {
       m.partials[3 * c] += s0;

@@ -311,7 +311,10 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   }
   int mc_wpb = 0, mc_ppw = 0;
   long long mc_smem = 0, mc_flops = 0;
-  const int mcv = ke.mc_variant ? ke.mc_variant() : 0;
+  // the fused MC kernel: its own default launch variant, or the requested one for the lane-group kernels
+  const char* env_v = getenv("QED_VARIANT");
+  const bool explicit_v = !use_regs && ((options && options->variant >= 0) || (env_v && *env_v));
+  const int mcv = explicit_v ? P->variant : (ke.mc_variant ? ke.mc_variant() : 0);
   ke.config(mcv, &mc_wpb, &mc_ppw, &mc_smem, &mc_flops);
 
   cudaError_t e = cudaGetDevice(&P->device);
@@ -331,7 +334,12 @@ qed_status qed_process_create_ex(const qed_state_spec* in, const qed_state_spec*
   // fused MC kernel: same per-point layout plus WPB x 3 doubles of block reduction space
   P->kern_mc = ke.mc_kernel(mcv);
   P->mc_wpb = mc_wpb;
-  P->smem_mc = mc_smem + 3LL * 8 * (mc_wpb * 32 / (1 << N));
+  // + the block reduction scratch (3 doubles per point of an eval pass) and the RAMBO staging (qed_mc_kernel.cuh:
+  // min(wpb * 32 / SUB, 8 PB) points per round, SUB = 4 / 8 / 16 lanes for N <= 4 / 8 / more, 4 (N + 2) + 2
+  // doubles each)
+  const int mc_sub = N <= 4 ? 4 : N <= 8 ? 8 : 16, mc_pb = std::max(1, mc_wpb * 32 / (1 << N));
+  const int mc_rb = std::min(mc_wpb * 32 / mc_sub, 8 * mc_pb);
+  P->smem_mc = mc_smem + 8LL * (3LL * mc_pb + (long long)mc_rb * (4 * (N + 2) + 2));
   e = cudaFuncSetAttribute(P->kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_mc);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaFuncSetAttribute(mc)"); }
   int bmc = 0;

@@ -260,7 +260,7 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
     if N in MMA_PROMOTE and mma_v:
         k = mma_v[MMA_PROMOTE[N]]
         vs = [vs[k]] + vs[:k] + vs[k + 1:]
-    mc_v = next(i for i, v in enumerate(vs) if not getattr(plans[v[0]], "mma", False))
+    mc_v = 0   # the fused MC kernel runs the eval default (tensor-core joins included; profiles/mc_sweep_r63.jsonl)
     fl = plan.flops
     flops_comment = "\n".join(f"//   {k:22s} {v:>10d}   (executed {plan.executed_flops[k]})" for k, v in fl.items())
     bodies = "\n".join(emit_plan_namespace(p, ns) for p, ns in zip(plans, nss))
@@ -272,10 +272,8 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
         f"    {'default' if i == 0 else f'case {i}'}: return per_config ? (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, true>\n"
         f"                                      : (const void*)qed::qed_eval_kernel<{nss[pi]}::T, {nss[pi]}::V{i}, false>;"
         for i, (pi, *_) in enumerate(vs))
-    # the fused MC kernel runs the CUDA-core joins (mc_variant): tensor-core variants map to that one
     mc_cases = "\n".join(
-        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{nss[vs[mc_v if getattr(plans[pi], 'mma', False) else i][0]]}::T, "
-        f"{nss[vs[mc_v if getattr(plans[pi], 'mma', False) else i][0]]}::V{mc_v if getattr(plans[pi], 'mma', False) else i}>;"
+        f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{nss[pi]}::T, {nss[pi]}::V{i}>;"
         for i, (pi, *_) in enumerate(vs))
     strides = ", ".join(str(plans[pi].stride) for pi, *_ in vs)
     flops = ", ".join(f"{plans[pi].flops_per_point}LL" for pi, *_ in vs)

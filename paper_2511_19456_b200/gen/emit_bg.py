@@ -206,11 +206,10 @@ def emit_bg_source(plan: BGPlan, extras: tuple = ()) -> str:
         f"                                      : (const void*)qed::qed_eval_kernel<{ns}::T, {ns}::V{k}, false>;"
         for i, (ns, k, _, _) in enumerate(allv))
     n = len(allv)
-    # the fused MC kernel runs the CUDA-core joins of the original default plan (its V0)
-    mcv = next(i for i, (ns, k, _, p) in enumerate(allv) if ns == f"qedbg_N{N}" and k == 0)
-    mns, mk = allv[mcv][0], allv[mcv][1]
-    mcases = "\n".join(f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<"
-                       f"{mns if getattr(p, 'mma', False) else ns}::T, {mns if getattr(p, 'mma', False) else ns}::V{mk if getattr(p, 'mma', False) else k}>;"
+    # the fused MC kernel runs the eval default too: with RAMBO batched per block (qed_mc_kernel.cuh) the promoted
+    # n = 4 tensor-core plan is the fastest MC plan as well (profiles/mc_sweep_r63.jsonl: 1.54e8 vs 1.47e8 points/s)
+    mcv = 0
+    mcases = "\n".join(f"    {'default' if i == 0 else f'case {i}'}: return (const void*)qed::qed_mc_kernel<{ns}::T, {ns}::V{k}>;"
                        for i, (ns, k, _, p) in enumerate(allv))
     return f"""// GENERATED by paper_2511_19456_b200/gen/emit_bg.py -- do not edit.
 // Berends-Giele (distributive rewrite of the node-reduced CDAG, NEXT #1) for N = {N} photons (n = {N - 1}):
@@ -269,8 +268,7 @@ CANDIDATES = {
 # n = 3 +4.9 %, n = 4 +3.8 % over the previous defaults -- at n = 5 the accumulator exchanges (one per subset,
 # against only one (sigma, tau) join each) cost more than the joins save: -16 %, -9 % with the one-shuffle
 # lane-tile exchange (r62), not kept; n = 7, 8 candidates
-# (SETB 3, 4, one-tile joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl).  The fused MC kernel
-# keeps the original default plan (qedbg_mc_variant_N*: the SETB 4 n = 4 plan measured 3.7 % slower inside MC)
+# (SETB 3, 4, one-tile joins) measured 2-26 % slower (profiles/sweep_r53_setb_n7n8.jsonl).
 PROMOTE = {4: (0, 2), 5: (2, 2), 6: (1, 1), 7: (0, 0)}
 
 
