@@ -238,7 +238,8 @@ def plan_variants(N: int) -> list[Plan]:
     if N == 5:
         plans.append(make_plan(N, store=1))
         # (r56: tensor-core joins with less shared memory per point -- level 2 recomputed per subset, or the
-        # 64-byte interior pitch -- measured 15-24 % slower than the default tensor-core plan: dropped)
+        # 64-byte interior pitch at 2 warps per block -- measured 15-24 % slower than the default tensor-core plan)
+        # (r65: the 64-byte pitch again at one warp per block, 9 resident points: -23 %, dropped)
         # (r38: the 64-byte spinor pitch, 22 KB per point and 10 resident points per SM, measured 11-16 % slower)
     return plans
 
@@ -251,6 +252,8 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
     for pi, p in enumerate(plans):
         if getattr(p, "mma", False):   # tensor-core joins: no accumulator split / sigma blocking; +- descriptor prefetch
             wpb, mb = choose_launch(p)
+            if p.G == 32 and wpb > 1:   # one point per block: the same residency in finer blocks
+                mb, wpb = mb * wpb, 1
             vs += [(pi, wpb, mb, 2, 2, 1, 1), (pi, wpb, mb, 2, 2, 1, 0)]
             if N <= 5:   # unrolled subset loop (UR); r60: n = 3 +5.6 %, n = 4 +0.8 %, n = 5 -28 % (20 subsets: code size)
                 vs += [(pi, wpb, mb, 2, 2, 1, 1, 1), (pi, wpb, mb, 2, 2, 1, 0, 1)]
