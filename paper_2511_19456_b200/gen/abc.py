@@ -116,19 +116,28 @@ def emit_cdag(N: int) -> tuple[str, int]:
             else:
                 L.append(f"  const double ou{_name(tau)} = {prev} * r{_name(rest)};")
                 flops += 1
-    # joins: one per diagram
-    L.append("  double M = 0.0;")
+    # joins: one per diagram, into NACC independent partial sums (a single accumulator makes the N! FMAs one
+    # dependent chain: latency-bound at N = 6), summed pairwise at the end
+    NACC = 4 if N >= 4 else 1
+    L.append("  double " + ", ".join(f"M{a} = 0.0" for a in range(NACC)) + ";")
+    d = 0
     for A in itertools.combinations(range(N), j):
         Ac = tuple(x for x in full if x not in A)
         for sig in itertools.permutations(A):
             for tau in itertools.permutations(Ac):
+                a = d % NACC
                 if N - j == 1:
-                    L.append(f"  M += in{_name(sig)};")
+                    L.append(f"  M{a} += in{_name(sig)};")
                     flops += 1
                 else:
-                    L.append(f"  M = fma(in{_name(sig)}, ou{_name(tau)}, M);")
+                    L.append(f"  M{a} = fma(in{_name(sig)}, ou{_name(tau)}, M{a});")
                     flops += 2
-    L.append("  return M;")
+                d += 1
+    if NACC == 4:
+        L.append("  return (M0 + M1) + (M2 + M3);")
+        flops += 3
+    else:
+        L.append("  return M0;")
     L.append("}")
     return "\n".join(L) + "\n", flops
 
