@@ -66,6 +66,17 @@ struct mma_of<T, decltype(void(T::MMA))> {
   static constexpr bool value = T::MMA;
 };
 
+// tensor-core CDAG plans with the u-bar leaves built and joined in T::TCH chunks of tau orderings (less shared
+// memory per point); every other plan reads 1
+template <class T, class = void>
+struct tch_of {
+  static constexpr int value = 1;
+};
+template <class T>
+struct tch_of<T, decltype(void(T::TCH))> {
+  static constexpr int value = T::TCH;
+};
+
 // ---- task kinds (one trie node x one helicity state); descriptor = (parent, eps, mask, out)
 template <class T>
 struct Tasks {
@@ -547,7 +558,7 @@ __device__ __forceinline__ void join_mma(const double* __restrict__ pbase, int l
       bim[tc] = v.i;
     }
 #pragma unroll 2
-    for (int tu = 0; tu < T::NTAU; ++tu) {
+    for (int tu = 0; tu < T::NTAU / tch_of<T>::value; ++tu) {   // the tau orderings of the resident chunk
 #pragma unroll
       for (int tr = 0; tr < TR; ++tr) {
         const c2 u = ld2(pbase + aos_slot<8>(T::UBL + (tu * T::NHO + tr * 8 + ri) * 8, c));
@@ -771,13 +782,39 @@ __device__ __forceinline__ double group_msq(const double (&amp)[2 * T::NAMP], in
   return a.norm * sum;
 }
 
+// joins of subset si (leaf buffer lb) for the warp's points, chunk by chunk of tau orderings (T::TCH; chunks
+// after the first are built here, between two group barriers), then the subset's accumulator bit exchange
+template <class T, int P>
+__device__ __forceinline__ void mma_subset_joins(double* smem, double* base, int g, int pb, int w, int lane, int half,
+                                                 int sg0, int sg1, int si, int lb,
+                                                 MmaAcc (&acc)[P][Mma<T>::TR][Mma<T>::TC]) {
+  constexpr bool SPLIT_SET = T::G > 32 && T::NSIG == 1;
+#pragma unroll
+  for (int ch = 0; ch < tch_of<T>::value; ++ch) {
+    if constexpr (tch_of<T>::value > 1) {
+      if (ch > 0) {
+        group_sync<T>(pb);                 // the previous chunk's u-bar leaves are joined
+        T::run_leaf_chunk(base, g, pb, si, ch);
+        group_sync<T>(pb);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const double* pbase = (T::G > 32 ? base : smem + (w * P + p) * T::STRIDE) + lb * T::LEAFB;
+      if (!SPLIT_SET || (si & 1) == half) join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (si + 1 < T::NSETS_REAL) T::mma_swap(acc[p], lane, si);
+}
+
 // the subset loop of mma_eval unrolled (launch field UR): batch B is a compile-time constant, so
 // T::mma_swap(acc, lane, si) folds to the one exchange of that subset
 template <class T, int DP, int P, int B, class SD>
 __device__ __forceinline__ void mma_batch(double* smem, double* base, int g, int pb, int w, int lane, int half, int sg0, int sg1,
                                           SD& sd, MmaAcc (&acc)[P][Mma<T>::TR][Mma<T>::TC]) {
   constexpr int s0 = B * T::SETB;
-  constexpr bool SPLIT_SET = T::G > 32 && T::NSIG == 1;
   if constexpr (DP) {
     T::run_set_d(base, g, pb, sd);
     group_sync<T>(pb);
@@ -789,14 +826,8 @@ __device__ __forceinline__ void mma_batch(double* smem, double* base, int g, int
 #pragma unroll
   for (int lb = 0; lb < T::SETB; ++lb) {
     const int si = s0 + lb;
-    if (si < T::NSETS_REAL) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const double* pbase = (T::G > 32 ? base : smem + (w * P + p) * T::STRIDE) + lb * T::LEAFB;
-        if (!SPLIT_SET || (si & 1) == half) join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
-        if (si + 1 < T::NSETS_REAL) T::mma_swap(acc[p], lane, si);
-      }
-    }
+    if (si < T::NSETS_REAL)
+      mma_subset_joins<T, P>(smem, base, g, pb, w, lane, half, sg0, sg1, si, lb, acc);
   }
   group_sync<T>(pb);
 }
@@ -815,6 +846,7 @@ __device__ __forceinline__ void mma_subsets(double* smem, double* base, int g, i
 template <class T, class V, int MODE>
 __device__ __forceinline__ double mma_eval(double* smem, double* base, int g, int pb, const QedEvalArgs& a, long long p0) {
   constexpr bool PER_CONFIG = MODE == 1;
+  static_assert(tch_of<T>::value == 1 || dp_of<V>::value == 0, "descriptor prefetch covers whole subsets only");
   constexpr int TR = Mma<T>::TR, TC = Mma<T>::TC, P = Mma<T>::P;
   constexpr int DP = dp_of<V>::value;
   const int lane = threadIdx.x & 31;
@@ -832,7 +864,7 @@ __device__ __forceinline__ double mma_eval(double* smem, double* base, int g, in
   // a 64-lane group: its two warps take half of the sigma rows (CDAG) or every other subset (Berends-Giele,
   // one sigma row); both apply every accumulator exchange
   const int half = T::G > 32 ? (threadIdx.x >> 5) & 1 : 0;
-  constexpr bool SPLIT_SIG = T::G > 32 && T::NSIG > 1, SPLIT_SET = T::G > 32 && T::NSIG == 1;
+  constexpr bool SPLIT_SIG = T::G > 32 && T::NSIG > 1;
   const int sg0 = SPLIT_SIG ? half * (T::NSIG / 2) : 0, sg1 = SPLIT_SIG ? sg0 + T::NSIG / 2 + (half ? T::NSIG % 2 : 0) : T::NSIG;
   typename sd_of<T, DP != 0>::type sd;
   if constexpr (DP) T::load_set(sd, g, 0);
@@ -852,14 +884,8 @@ __device__ __forceinline__ double mma_eval(double* smem, double* base, int g, in
 #pragma unroll
     for (int lb = 0; lb < T::SETB; ++lb) {
       const int si = s0 + lb;
-      if (T::NSETS_REAL % T::SETB == 0 || si < T::NSETS_REAL) {   // padding subsets: leaves only
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const double* pbase = (T::G > 32 ? base : smem + (w * P + p) * T::STRIDE) + lb * T::LEAFB;
-          if (!SPLIT_SET || (si & 1) == half) join_mma<T>(pbase, lane, sg0, sg1, acc[p]);
-          if (si + 1 < T::NSETS_REAL) T::mma_swap(acc[p], lane, si);
-        }
-      }
+      if (T::NSETS_REAL % T::SETB == 0 || si < T::NSETS_REAL)   // padding subsets: leaves only
+        mma_subset_joins<T, P>(smem, base, g, pb, w, lane, half, sg0, sg1, si, lb, acc);
     }
     group_sync<T>(pb);
   }

@@ -125,6 +125,23 @@ def _tasks(name, tasks):
 KIND_FN = {"vs_col": "vs_col", "vs_row": "vs_row", "phi": "phi", "ub": "ub"}
 
 
+def _chunk_members(tch: int, chunk_lines: list[str]) -> str:
+    """Traits members of a tau-chunked tensor-core plan: TCH and the leaf chunks after the first."""
+    if tch == 1:
+        return ""
+    body = "\n".join(chunk_lines)
+    return f"""  // u-bar leaves built and joined in TCH chunks of tau orderings (make_plan(tau_chunks=...))
+  static constexpr int TCH = {tch};
+  static __device__ __forceinline__ void run_leaf_chunk(double* base, int g, int pb, int si, int ch) {{
+    (void)pb;
+    switch (ch) {{
+{body}
+      default: break;
+    }}
+  }}
+"""
+
+
 def emit_plan_namespace(plan: Plan, ns: str) -> str:
     """Task tables + traits struct T of one lowered plan, in namespace `ns`."""
     N, L = plan.N, plan.layout
@@ -152,7 +169,19 @@ def emit_plan_namespace(plan: Plan, ns: str) -> str:
                 set_flat += t
     lines, off = [], 0
     sd_fields, ld_lines, ex_lines = [], [], []
+    tch = getattr(plan, "tau_chunks", 1)
+    chunk_lines = []                 # tau-chunked tensor-core plans: the leaf chunks after the first
+    n_main = len(struct) - (tch - 1)
     for i, st in enumerate(struct):
+        if i >= n_main:
+            c_lines = []
+            for q, (kind, cnt) in enumerate(st):
+                kid = {"vs_col": 0, "vs_row": 1, "phi": 2, "ub": 3}[kind]
+                c_lines.append(f"qed::run_tasks<T, {cnt}, qed::TaskFn<T, {kid}>, 0>(base, g, "
+                               f"k_set_tasks + si * {per_set} + {off}, qed::TaskFn<T, {kid}>{{}});")
+                off += cnt
+            chunk_lines.append(f"      case {i - n_main + 1}: " + " ".join(c_lines) + " break;")
+            continue
         if i > 0:
             lines.append("    qed::group_sync<T>(pb);")
             ex_lines.append("    qed::group_sync<T>(pb);")
@@ -196,7 +225,7 @@ struct T {{
   static constexpr int NSETS = {len(plan.sets)}, NSETS_REAL = NSETS, SETB = 1, LEAFB = 0;
   static constexpr int HS = 1, NAMP = 4;
   static constexpr long long FLOPS_PER_POINT = {plan.flops_per_point}LL;
-{_mma_members(plan) if getattr(plan, "mma", False) else ""}
+{_mma_members(plan) if getattr(plan, "mma", False) else ""}{_chunk_members(tch, chunk_lines)}
   static __device__ __forceinline__ unsigned set_mask(int si) {{ return k_set_mask[si]; }}
   static __device__ __forceinline__ int set_pos(int si, int i) {{ return k_set_pos[si * N + i]; }}
   static __device__ __forceinline__ unsigned hiho(int si, int g) {{ return __ldg(k_hiho + si * G + g); }}
@@ -235,6 +264,9 @@ def plan_variants(N: int) -> list[Plan]:
     plans = [make_plan(N)]
     if N in (4, 5, 6):
         plans.append(make_plan(N, mma=True))
+    # (r68: u-bar leaves built and joined in 2 or 3 chunks of tau orderings -- 12-16 % less shared memory per
+    # point, 1-2 more resident points per SM -- measured 4-28 % slower at n = 4, 5: the extra leaf phases and
+    # barriers cost more than the occupancy gains; make_plan(tau_chunks=...) is kept, not compiled)
     if N == 5:
         plans.append(make_plan(N, store=1))
         # (r56: tensor-core joins with less shared memory per point -- level 2 recomputed per subset, or the
@@ -254,6 +286,9 @@ def emit_source(plan: Plan, extra: list[Plan] | None = None) -> str:
             wpb, mb = choose_launch(p)
             if p.G == 32 and wpb > 1:   # one point per block: the same residency in finer blocks
                 mb, wpb = mb * wpb, 1
+            if getattr(p, "tau_chunks", 1) > 1:   # leaf chunks between joins: no descriptor prefetch (whole subsets)
+                vs += [(pi, wpb, mb, 2, 2, 1, 0), (pi, wpb, mb, 2, 2, 1, 0, 1)]
+                continue
             vs += [(pi, wpb, mb, 2, 2, 1, 1), (pi, wpb, mb, 2, 2, 1, 0)]
             if N <= 5:   # unrolled subset loop (UR); r60: n = 3 +5.6 %, n = 4 +0.8 %, n = 5 -28 % (20 subsets: code size)
                 vs += [(pi, wpb, mb, 2, 2, 1, 1, 1), (pi, wpb, mb, 2, 2, 1, 0, 1)]

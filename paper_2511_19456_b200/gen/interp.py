@@ -110,15 +110,22 @@ def _mma_join(plan, sm, run, get_aos_sp8):
     N, L = plan.N, plan.layout
     R, C = plan.n_ho, plan.n_hi
     acc = np.zeros((R, C), dtype=complex)
+    TCH = getattr(plan, "tau_chunks", 1)
+    NT = plan.n_tau // TCH
     for si, A in enumerate(plan.sets):
-        for stage in plan.set_stages[si]:
+        stages = plan.set_stages[si]
+        for stage in stages[:len(stages) - TCH + 1]:      # recomputed levels and leaf chunk 0 (phi + ubar)
             for kind, tasks in stage:
                 run(kind, tasks)
-        U = np.array([[get_aos_sp8(L["UBL"] + (t * R + r) * 8) for r in range(R)] for t in range(plan.n_tau)])
-        P = np.array([[get_aos_sp8(L["PHI"] + (s_ * C + c) * 8) for c in range(C)] for s_ in range(plan.n_sigma)])
-        for t in range(plan.n_tau):
-            for s_ in range(plan.n_sigma):
-                acc += U[t] @ P[s_].T
+        for c in range(TCH):
+            if c:
+                for kind, tasks in stages[len(stages) - TCH + c]:
+                    run(kind, tasks)
+            U = np.array([[get_aos_sp8(L["UBL"] + (t * R + r) * 8) for r in range(R)] for t in range(NT)])
+            P = np.array([[get_aos_sp8(L["PHI"] + (s_ * C + c_) * 8) for c_ in range(C)] for s_ in range(plan.n_sigma)])
+            for t in range(NT):
+                for s_ in range(plan.n_sigma):
+                    acc += U[t] @ P[s_].T
         if si + 1 < len(plan.sets):
             pa, pc = plan.mma_swaps[si]
             (_, ba), (_, bc) = MMA_BIT[pa], MMA_BIT[pc]

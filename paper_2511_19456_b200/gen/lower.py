@@ -185,7 +185,7 @@ def mma_assignments(N: int, j: int, order: list[tuple[int, ...]]):
 
 
 def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | None = None,
-              mma: bool = False) -> Plan:
+              mma: bool = False, tau_chunks: int = 1) -> Plan:
     if N < 2:
         raise ValueError("need at least two photons (n >= 1)")
     if j is None:
@@ -231,9 +231,11 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
         alloc(f"SOUT{i}", perm_count(N - j, i) * (1 << (i + 1)) * SP, 8)
     n_sigma, n_tau = math.factorial(j), math.factorial(N - j)
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
-    if mma:   # AoS leaves (64-byte pitch, XOR component swizzle): spinor (row, slot) at row * NH + slot
+    assert tau_chunks == 1 or (mma and n_tau % tau_chunks == 0)
+    if mma:   # AoS leaves (64-byte pitch, XOR component swizzle): spinor (row, slot) at row * NH + slot; with
+        # tau_chunks > 1 the u-bar leaves of one chunk of tau orderings at a time (joined chunk by chunk)
         alloc("PHI", n_sigma * n_hi * 8, 8)
-        alloc("UBL", n_tau * n_ho * 8, 8)
+        alloc("UBL", n_tau // tau_chunks * n_ho * 8, 8)
     else:
         alloc("PHI", n_sigma * 4 * n_hi * 2, 8)
         alloc("UBL", n_tau * 4 * n_ho * 2, 8)
@@ -259,6 +261,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
     plan = Plan(N=N, j=j, G=G, store=store, sets=[], sigmas=[], taus=[], layout=lay, stride=stride)
     plan.sp = SP
     plan.mma = mma
+    plan.tau_chunks = tau_chunks
     order = johnson_order(N, j) if mma else list(itertools.combinations(range(N), j))
     if mma:
         plan.mma_assign, plan.mma_swaps = mma_assignments(N, j, order)
@@ -358,14 +361,19 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
                 parent = lay["UB"] + (ho & 1) * SP if L == 1 else out_off(tu[:-1], hpar, local_out)
                 if mma:
                     sl = mma_slot(plan.mma_assign[si_], Ac, ho, MMA_ROW_POS)
-                    dst = lay["UBL"] + (ti * n_ho + sl) * 8
+                    dst = lay["UBL"] + ((ti % (n_tau // tau_chunks)) * n_ho + sl) * 8
                 else:
                     dst = leaf_off(lay["UBL"], n_ho, ti, ho)
                 ub.append((parent, eps_off(tu[-1], lam[tu[-1]]), 0, dst))
         if mma:   # consecutive lanes store consecutive AoS spinors (conflict-free with the XOR swizzle)
             phi.sort(key=lambda t: t[3])
-            ub.sort(key=lambda t: t[3])
-        stages.append([("phi", phi), ("ub", ub)])
+            per = len(ub) // tau_chunks          # ub was built tau-major: chunk c = taus c * per / n_ho ..
+            chunks = [sorted(ub[c * per:(c + 1) * per], key=lambda t: t[3]) for c in range(tau_chunks)]
+            stages.append([("phi", phi), ("ub", chunks[0])])
+            for c in range(1, tau_chunks):       # leaf chunk stages: each follows the joins of the previous chunk
+                stages.append([("ub", chunks[c])])
+        else:
+            stages.append([("phi", phi), ("ub", ub)])
         plan.set_stages.append(stages)
 
     # ---------------------------------------------------------------- algorithmic flops per point

@@ -324,7 +324,7 @@ def test_johnson_order_exchanges_one_photon_per_step():
                 assert len(set(asg.values())) == N
 
 
-@pytest.mark.parametrize("N,bg", [(4, False), (5, False), (6, False), (4, True), (5, True), (6, True)])
+@pytest.mark.parametrize("N,bg", [(4, False), (5, False), (6, False), (4, True), (5, True), (6, True), (5, "tc2")])
 def test_mma_plans_interpreted_match_oracle(N, bg):
     """Tensor-core-join plans (AoS leaves at their accumulator slot, Johnson order, per-subset bit exchanges,
     final configuration map), executed by the interpreter with the kernel's rules, give the oracle's
@@ -333,7 +333,10 @@ def test_mma_plans_interpreted_match_oracle(N, bg):
     from paper_2511_19456_b200.gen.lower import make_plan
     from paper_2511_19456_b200.gen.lower_bg import make_bg_plan
     n = N - 1
-    plan = make_bg_plan(N, mma=True) if bg else make_plan(N, mma=True)
+    if bg == "tc2":   # u-bar leaves in two chunks of tau orderings (make_plan(tau_chunks=2))
+        plan, bg = make_plan(N, mma=True, tau_chunks=2), False
+    else:
+        plan = make_bg_plan(N, mma=True) if bg else make_plan(N, mma=True)
     mom = synthetic.rambo_cm(n, 2, sqrt_s=5.0, seed=1000 + n).numpy()
     A = oracle.amps(1, n, mom)
     for k in range(2):
