@@ -232,6 +232,7 @@ def make_plan(N: int, j: int | None = None, store: int | None = None, sp: int | 
     n_sigma, n_tau = math.factorial(j), math.factorial(N - j)
     n_hi, n_ho = 1 << (j + 1), 1 << (N - j + 1)
     assert tau_chunks == 1 or (mma and n_tau % tau_chunks == 0)
+    assert not mma or (n_hi >= 8 and n_ho >= 8), "tensor-core tiles are 8 x 8: both sides need >= 2 photons"
     if mma:   # AoS leaves (64-byte pitch, XOR component swizzle): spinor (row, slot) at row * NH + slot; with
         # tau_chunks > 1 the u-bar leaves of one chunk of tau orderings at a time (joined chunk by chunk)
         alloc("PHI", n_sigma * n_hi * 8, 8)

@@ -279,8 +279,8 @@ def make_bg_plan(N: int, j: int | None = None, setb: int | None = None, store: i
     SP = sp if sp is not None else PITCH_BG.get(N, 10)
     grp = tuple(grp) if grp is not None else (0, 0, 0, 0, 0)
     grouped = any(grp)
-    if mma:   # tensor-core joins (qed_eval_kernel.cuh mma_eval): one-tile joins, ungrouped tasks
-        assert not grouped and (hs in (None, 1)) and j <= len(MMA_COL_POS) and N - j <= len(MMA_ROW_POS)
+    if mma:   # tensor-core joins (qed_eval_kernel.cuh mma_eval): one-tile joins, ungrouped tasks; 8 x 8 tiles
+        assert not grouped and (hs in (None, 1)) and 2 <= j <= len(MMA_COL_POS) and 2 <= N - j <= len(MMA_ROW_POS)
         hs = 1
     if store is None:
         store = default_bg_store(N, j)
