@@ -245,6 +245,26 @@ def traffic_from_profile(n: int, points: int):
         return None
 
 
+def l1_roofline(algorithm: str, n: int, points: int, seconds: float):
+    """Second roofline for the lane-group Berends-Giele kernels, which are bound by the L1 data pipe (shared +
+    global LSU wavefronts, 1 per clock per SM; DESIGN.md §6 kernel 2b) rather than by FP64: wavefronts per
+    point from the committed ncu --set full summary (profiles/ncu_l1.json, tools/summarize_raw.py) x the points
+    of this launch / its live CUDA-event duration, against 148 SM x 1965 MHz wavefronts/s."""
+    if algorithm != "bg":
+        return None
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "ncu_l1.json"))).get(f"s3_bg{n}")
+    except Exception:
+        return None
+    if not rec:
+        return None
+    peak = 148 * 1.965e9
+    achieved = rec["l1_wavefronts_per_point"] * points / seconds
+    return {"bound": "l1", "unit": "wavefronts/s", "wavefronts_per_point": rec["l1_wavefronts_per_point"],
+            "achieved": round(achieved, -6), "peak": peak, "frac": round(achieved / peak, 4),
+            "ncu_l1_data_pipe_pct": rec["l1_data_pipe_pct"], "source": f"profiles/ncu_l1.json s3_bg{n} ({rec['points']} points)"}
+
+
 # ---------------------------------------------------------------- oracle timings (CPU)
 def oracle_rate(n: int, target_s: float, sqrt_s: float, seed: int) -> dict:
     import oracle
@@ -435,6 +455,9 @@ def sweep_per_n(args, world, stream, dev, algorithm: str, paper_direction: bool 
                        "ms_per_step": 1e3 * tm / K, "flops_per_point": fm,
                        "achieved_tflops": round(fm * Pm / ks / 1e12, 3),
                        "frac_fp64_peak": round(fm * Pm / ks / 1e12 / FP64_PEAK_TFLOPS, 4)}
+        l1 = l1_roofline(algorithm, m, Pm, ks)
+        if l1:
+            out[str(m)]["l1_roofline"] = l1
         del sm, om, pm
     return out
 
@@ -492,20 +515,31 @@ def hbm_peak_gbs() -> float:
 
 
 def run_e2e(args, world, proc, soa, P) -> dict:
-    """Same metric through the public host-buffer API (qed_eval_msq_host): every step copies the
-    step's momenta H2D from pinned memory, evaluates, and copies |M|^2 back D2H."""
+    """Same metric through the public host-buffer API: every step copies the step's momenta H2D from
+    pinned memory, evaluates, and copies |M|^2 back D2H.  The line's value is
+    qed_eval_msq_host_ex(QED_HOST_ONSHELL) -- the 3-momenta cross PCIe, the energies are restored on the
+    device from the mass shell -- and "full_4momenta" is qed_eval_msq_host (all 4 components uploaded)."""
     import torch
     h_soa = soa.cpu().pin_memory()
     h_out = torch.empty(P, dtype=torch.float64).pin_memory()
-    for _ in range(max(1, args.warmup)):
-        proc.eval_msq_host(h_soa, h_out, P)
-    barrier(world)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        proc.eval_msq_host(h_soa, h_out, P)
-    e2e_s = max_over_ranks(world, time.perf_counter() - t)
+
+    def timed(onshell):
+        for _ in range(max(1, args.warmup)):
+            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell)
+        barrier(world)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell)
+        return max_over_ranks(world, time.perf_counter() - t)
+
+    full_s = timed(False)
+    e2e_s = timed(True)
+    rows3 = 3 * (h_soa.shape[0] // 4)   # momentum rows uploaded per step (energies restored on the device)
     return {"value": world * P * args.steps / e2e_s, "unit": UNIT,
-            "h2d_bytes_per_step": int(h_soa.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8)}
+            "h2d_bytes_per_step": int(rows3 * P * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
+            "api": "qed_eval_msq_host_ex(QED_HOST_ONSHELL)",
+            "full_4momenta": {"value": world * P * args.steps / full_s, "unit": UNIT,
+                              "h2d_bytes_per_step": int(h_soa.numel() * 8), "api": "qed_eval_msq_host"}}
 
 def run_b200(args, world, rank, local):
     import torch

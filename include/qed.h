@@ -125,6 +125,17 @@ qed_status qed_eval_msq_configs(const qed_process* proc, const double* momenta, 
 qed_status qed_eval_msq_host(const qed_process* proc, const double* momenta_host, int64_t n_points,
                              double* out_host);
 
+/* qed_eval_msq_host with upload flags (extension).  flags = 0 is qed_eval_msq_host.
+   QED_HOST_ONSHELL: the energy rows momenta[4*j*n_points ...] are NOT read or uploaded.  Only the
+   3-momenta cross PCIe (3/4 of the bytes), and a device kernel restores every energy from the
+   mass shell the header's conventions already require, E_j = sqrt(|p_j|^2 + m_j^2) with m = m_e = 1
+   for the electrons and 0 for the photons (§1.4 line 62: on-shell external states), before
+   the |M|^2 kernel runs on the chunk.  Results then differ from flags = 0 by the rounding of the
+   given energies (relative ~1e-15 for RAMBO inputs).  Unknown flag bits: QED_ERR_INVALID_ARGUMENT. */
+#define QED_HOST_ONSHELL 1u
+qed_status qed_eval_msq_host_ex(const qed_process* proc, const double* momenta_host, int64_t n_points,
+                                double* out_host, uint32_t flags);
+
 /* Monte-Carlo cross-section partial sums.
    Generates points first_index .. first_index + n_points - 1 of the phase-space
    sequence keyed by seed (Philox4x32-10, counter = global point index, so the

@@ -159,6 +159,22 @@ qed_status check_device(int device) {
 
 constexpr long long kHostChunkMin = 1LL << 18;   // points per pipelined chunk of qed_eval_msq_host (minimum)
 
+// QED_HOST_ONSHELL (include/qed.h): restore the energy rows of one uploaded chunk from the mass shell,
+// E_j = sqrt(|p_j|^2 + m_j^2), m = 1 for the particles in electron_mask (bit j), 0 for the photons.
+// One thread per (point, particle), consecutive threads on consecutive points: coalesced 8-byte rows.
+__global__ void __launch_bounds__(256) qed_onshell_energy_kernel(double* __restrict__ mom, long long cnt, int n_ext,
+                                                                 unsigned electron_mask) {
+  const long long total = cnt * n_ext;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(t / cnt);
+    const long long i = t - (long long)j * cnt;
+    double* r = mom + (long long)(4 * j) * cnt + i;
+    const double px = r[cnt], py = r[2 * cnt], pz = r[3 * cnt];
+    const double m2 = ((electron_mask >> j) & 1u) ? 1.0 : 0.0;
+    r[0] = sqrt(fma(px, px, fma(py, py, fma(pz, pz, m2))));
+  }
+}
+
 struct qed_process {
   int n = 0, N = 0, n_in_ph = 0, n_out_ph = 0, n_ext = 0;
   qed::QedEvalArgs args{};
@@ -395,8 +411,15 @@ qed_status qed_eval_msq_configs(const qed_process* proc, const double* momenta, 
 
 qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_host, int64_t n_points,
                              double* out_host) {
+  return qed_eval_msq_host_ex(cproc, momenta_host, n_points, out_host, 0u);
+}
+
+qed_status qed_eval_msq_host_ex(const qed_process* cproc, const double* momenta_host, int64_t n_points,
+                                double* out_host, uint32_t flags) {
   qed_process* P = const_cast<qed_process*>(cproc);
   if (!P) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
+  if (flags & ~QED_HOST_ONSHELL) return fail(QED_ERR_INVALID_ARGUMENT, "unknown flag bits in qed_eval_msq_host_ex");
+  const bool onshell = (flags & QED_HOST_ONSHELL) != 0;
   if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
   if (n_points == 0) return QED_OK;
   if (!momenta_host || !out_host) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
@@ -444,16 +467,31 @@ qed_status qed_eval_msq_host(const qed_process* cproc, const double* momenta_hos
     const long long cnt = std::min<long long>(chunk, n_points - i0);
     cudaStream_t st = P->hstream[b];
     const size_t spitch = sizeof(double) * (size_t)n_points;
-    if (spitch <= (size_t)max_pitch) {
-      e = cudaMemcpy2DAsync(P->d_mom[b], sizeof(double) * (size_t)cnt, momenta_host + i0, spitch,
-                            sizeof(double) * (size_t)cnt, rows, cudaMemcpyHostToDevice, st);
-    } else {   // source pitch above the device limit (~2^28 points): one copy per SoA row
-      e = cudaSuccess;
-      for (int r = 0; r < rows && e == cudaSuccess; ++r)
-        e = cudaMemcpyAsync(P->d_mom[b] + (size_t)r * cnt, momenta_host + (size_t)r * n_points + i0,
-                            sizeof(double) * (size_t)cnt, cudaMemcpyHostToDevice, st);
+    // row blocks to upload: all rows, or (ONSHELL) the 3 momentum rows 4j+1..4j+3 of every particle j
+    const int nblk = onshell ? P->n_ext : 1, blk_rows = onshell ? 3 : rows;
+    e = cudaSuccess;
+    for (int k = 0; k < nblk && e == cudaSuccess; ++k) {
+      const int r0 = onshell ? 4 * k + 1 : 0;
+      if (spitch <= (size_t)max_pitch) {
+        e = cudaMemcpy2DAsync(P->d_mom[b] + (size_t)r0 * cnt, sizeof(double) * (size_t)cnt,
+                              momenta_host + (size_t)r0 * n_points + i0, spitch, sizeof(double) * (size_t)cnt,
+                              blk_rows, cudaMemcpyHostToDevice, st);
+      } else {   // source pitch above the device limit (~2^28 points): one copy per SoA row
+        for (int r = r0; r < r0 + blk_rows && e == cudaSuccess; ++r)
+          e = cudaMemcpyAsync(P->d_mom[b] + (size_t)r * cnt, momenta_host + (size_t)r * n_points + i0,
+                              sizeof(double) * (size_t)cnt, cudaMemcpyHostToDevice, st);
+      }
     }
     if (e != cudaSuccess) return drain(cuda_fail(e, "H2D copy"));
+    if (onshell) {
+      const unsigned emask = 1u | (1u << P->args.e_out_particle);
+      const long long work = cnt * P->n_ext;
+      const int grid = (int)std::min<long long>((work + 255) / 256, 8LL * P->num_sms);
+      qed_onshell_energy_kernel<<<grid, 256, 0, st>>>(P->d_mom[b], cnt, P->n_ext, emask);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return drain(cuda_fail(e, "on-shell energy kernel launch"));
+      g_launches.fetch_add(1);
+    }
     qed_status stt = launch_eval(P, P->d_mom[b], cnt, P->d_out[b], st, 0);
     if (stt != QED_OK) return drain(stt);
     e = cudaMemcpyAsync(out_host + i0, P->d_out[b], sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToHost, st);

@@ -16,11 +16,12 @@ LIB_PATH = os.path.join(_PKG, "lib", "libqed.so")
 QED_OK = 0
 QED_SUM = -1
 MC_CHUNK = 1024
+HOST_ONSHELL = 1   # QED_HOST_ONSHELL (include/qed.h)
 _STATUS = {0: "QED_OK", 1: "QED_ERR_INVALID_ARGUMENT", 2: "QED_ERR_UNSUPPORTED", 3: "QED_ERR_CUDA",
            4: "QED_ERR_OUT_OF_MEMORY", 5: "QED_ERR_INTERNAL"}
 
 EXPORTED = ["qed_process_create", "qed_process_create_ex", "qed_process_destroy", "qed_eval_msq", "qed_eval_msq_configs",
-            "qed_eval_msq_host", "qed_mc_sum", "qed_get_process_info", "qed_last_error", "qed_launch_count"]
+            "qed_eval_msq_host", "qed_eval_msq_host_ex", "qed_mc_sum", "qed_get_process_info", "qed_last_error", "qed_launch_count"]
 EXPORTED_ABC = ["abc_process_create", "abc_process_destroy", "abc_eval_msq", "abc_get_process_info"]
 
 
@@ -81,6 +82,7 @@ def _load() -> ctypes.CDLL:
     lib.qed_eval_msq.argtypes = [vp, vp, i64, vp, vp]
     lib.qed_eval_msq_configs.argtypes = [vp, vp, i64, vp, vp]
     lib.qed_eval_msq_host.argtypes = [vp, vp, i64, vp]
+    lib.qed_eval_msq_host_ex.argtypes = [vp, vp, i64, vp, ctypes.c_uint32]
     lib.qed_mc_sum.argtypes = [vp, ctypes.POINTER(_McConfig), vp, vp]
     lib.qed_get_process_info.argtypes = [vp, ctypes.POINTER(ProcessInfo)]
     lib.abc_process_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
@@ -216,11 +218,17 @@ class Process:
                                          _ptr(out, n_points * H, "out", self.device), _stream_ptr(stream)),
                "qed_eval_msq_configs")
 
-    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int | None = None) -> None:
-        """Host buffers (pinned recommended): momenta [(4*n_ext), n_points], out [n_points]."""
+    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int | None = None, onshell: bool = False) -> None:
+        """Host buffers (pinned recommended): momenta [(4*n_ext), n_points], out [n_points].
+        onshell=True: qed_eval_msq_host_ex(QED_HOST_ONSHELL), only the 3-momenta are uploaded and the
+        energies are restored on the device from the mass shell (include/qed.h)."""
         n_points = out_host.numel() if n_points is None else n_points
-        _check(_lib.qed_eval_msq_host(self._h, self._soa(momenta_soa_host, n_points, None), n_points,
-                                      _ptr(out_host, n_points, "out", None)), "qed_eval_msq_host")
+        mom = self._soa(momenta_soa_host, n_points, None)
+        out = _ptr(out_host, n_points, "out", None)
+        if onshell:
+            _check(_lib.qed_eval_msq_host_ex(self._h, mom, n_points, out, HOST_ONSHELL), "qed_eval_msq_host_ex")
+        else:
+            _check(_lib.qed_eval_msq_host(self._h, mom, n_points, out), "qed_eval_msq_host")
 
     def mc_sum(self, partials, sqrt_s: float, omega_min: float, seed: int, first_index: int, n_points: int,
                stream=None) -> None:

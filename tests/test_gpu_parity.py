@@ -243,6 +243,40 @@ def test_host_entry_point_pipelined_chunks(qed):
     assert torch.equal(out2, out)
 
 
+@pytest.mark.parametrize("n,n_in,algorithm", [(2, 1, "cdag"), (3, 3, "bg")])
+def test_host_entry_point_onshell(qed, n, n_in, algorithm):
+    """qed_eval_msq_host_ex(QED_HOST_ONSHELL): only the 3-momenta are uploaded and the energies are
+    restored on the device from the mass shell (include/qed.h).  The host energy rows are poisoned with
+    NaN to prove they are not read; oracle on the original momenta, over pipelined chunks with a
+    ragged tail, in the north-star and the paper direction (electron rows 0 and n_in + 1)."""
+    P = 2 * (1 << 18) + 777
+    mom = synthetic.rambo_cm(n if n_in == 1 else n, P, sqrt_s=5.0, seed=8200 + n).numpy()
+    if n_in > 1:   # time-reversed north-star kinematics (test_paper_direction_matches_oracle)
+        mom = np.concatenate([mom[:, 2:3], mom[:, 3:], mom[:, 0:1], mom[:, 1:2]], axis=1)
+    soa = synthetic.to_soa(torch.from_numpy(mom))
+    dev = torch.empty(P, dtype=torch.float64, device="cuda")
+    proc = qed.Process(n, n_in_photons=n_in, algorithm=algorithm)
+    proc.eval_msq(soa.cuda(), dev)
+    torch.cuda.synchronize()
+    poisoned = soa.clone()
+    poisoned[0::4] = float("nan")
+    out = torch.full((P,), float("nan"), dtype=torch.float64).pin_memory()
+    proc.eval_msq_host(poisoned.pin_memory(), out, P, onshell=True)
+    got = out.numpy()
+    assert np.all(np.isfinite(got))
+    # same points as the device path up to the rounding of the given energies, amplified by the
+    # conditioning of the propagator denominators (Q^2 - m^2 cancels): ~1e-15 typical, 5.5e-12 worst (r s3b)
+    dev_rel = np.abs(got / dev.cpu().numpy() - 1)
+    assert np.max(dev_rel) <= TOL
+    worst = np.argsort(dev_rel)[-16:]
+    idx = np.unique(np.concatenate([np.arange(0, 40), np.arange((1 << 18) - 40, (1 << 18) + 40), np.arange(P - 40, P),
+                                    worst]))
+    ref = oracle.msq(n_in, n + 1 - n_in, mom[idx])
+    assert np.max(np.abs(got[idx] / ref - 1)) <= TOL
+    with pytest.raises(qed.QedError):
+        qed._check(qed._lib.qed_eval_msq_host_ex(proc._h, poisoned.data_ptr(), P, out.data_ptr(), 2), "flags")
+
+
 def test_two_streams_two_handles(qed):
     n = 2
     mom = synthetic.rambo_cm(n, 20000, seed=9000)
