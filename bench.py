@@ -523,21 +523,26 @@ def run_e2e(args, world, proc, soa, P) -> dict:
     h_soa = soa.cpu().pin_memory()
     h_out = torch.empty(P, dtype=torch.float64).pin_memory()
 
-    def timed(onshell):
+    def timed(onshell, conserve):
         for _ in range(max(1, args.warmup)):
-            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell)
+            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell, conserve=conserve)
         barrier(world)
         t = time.perf_counter()
         for _ in range(args.steps):
-            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell)
+            proc.eval_msq_host(h_soa, h_out, P, onshell=onshell, conserve=conserve)
         return max_over_ranks(world, time.perf_counter() - t)
 
-    full_s = timed(False)
-    e2e_s = timed(True)
-    rows3 = 3 * (h_soa.shape[0] // 4)   # momentum rows uploaded per step (energies restored on the device)
+    full_s = timed(False, False)
+    on_s = timed(True, False)
+    e2e_s = timed(True, True)
+    n_ext = h_soa.shape[0] // 4
+    # momentum rows uploaded per step: 3 per particle (energies restored on the device), the outgoing
+    # electron's none (momentum conservation)
     return {"value": world * P * args.steps / e2e_s, "unit": UNIT,
-            "h2d_bytes_per_step": int(rows3 * P * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
-            "api": "qed_eval_msq_host_ex(QED_HOST_ONSHELL)",
+            "h2d_bytes_per_step": int(3 * (n_ext - 1) * P * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
+            "api": "qed_eval_msq_host_ex(QED_HOST_ONSHELL | QED_HOST_CONSERVE)",
+            "onshell_3momenta": {"value": world * P * args.steps / on_s, "unit": UNIT,
+                                 "h2d_bytes_per_step": int(3 * n_ext * P * 8), "api": "qed_eval_msq_host_ex(QED_HOST_ONSHELL)"},
             "full_4momenta": {"value": world * P * args.steps / full_s, "unit": UNIT,
                               "h2d_bytes_per_step": int(h_soa.numel() * 8), "api": "qed_eval_msq_host"}}
 

@@ -131,8 +131,14 @@ qed_status qed_eval_msq_host(const qed_process* proc, const double* momenta_host
    mass shell the header's conventions already require, E_j = sqrt(|p_j|^2 + m_j^2) with m = m_e = 1
    for the electrons and 0 for the photons (§1.4 line 62: on-shell external states), before
    the |M|^2 kernel runs on the chunk.  Results then differ from flags = 0 by the rounding of the
-   given energies (relative ~1e-15 for RAMBO inputs).  Unknown flag bits: QED_ERR_INVALID_ARGUMENT. */
+   given energies (relative ~1e-15 for RAMBO inputs, up to ~1e-11 where propagator denominators cancel).
+   QED_HOST_CONSERVE (only together with QED_HOST_ONSHELL): the outgoing electron's rows are not read or
+   uploaded either; the device restores its 3-momentum from the 4-momentum conservation the header's
+   conventions require, p' = p + sum(incoming k) - sum(outgoing k), then its energy from the shell
+   (4/5 of the ONSHELL bytes at n = 2).  Unknown flag bits, or CONSERVE without ONSHELL:
+   QED_ERR_INVALID_ARGUMENT. */
 #define QED_HOST_ONSHELL 1u
+#define QED_HOST_CONSERVE 2u
 qed_status qed_eval_msq_host_ex(const qed_process* proc, const double* momenta_host, int64_t n_points,
                                 double* out_host, uint32_t flags);
 

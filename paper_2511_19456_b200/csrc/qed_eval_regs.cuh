@@ -245,10 +245,13 @@ __global__ void __launch_bounds__(V::WPB * 32, V::MIN_BLOCKS) qed_regs_kernel(Qe
           }
         }
       } else if (a.fixed_mask == 0) {
-        double part = 0.0;
+        // four interleaved partial sums: one chain of 2 NACC dependent DFMAs held the pass's tail
+        // (3.2 % of the n = 2 stall samples, profiles/r02/lines_n2.txt)
+        double part[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int idx = 0; idx < NACC; ++idx) part = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], part));
-        if (T::config_of(0, sub_) != 0xffffffffu) sum += part;
+        for (int idx = 0; idx < NACC; ++idx)
+          part[idx & 3] = fma(acc[2 * idx], acc[2 * idx], fma(acc[2 * idx + 1], acc[2 * idx + 1], part[idx & 3]));
+        if (T::config_of(0, sub_) != 0xffffffffu) sum += (part[0] + part[1]) + (part[2] + part[3]);
       } else {
 #pragma unroll
         for (int idx = 0; idx < NACC; ++idx) {

@@ -159,19 +159,32 @@ qed_status check_device(int device) {
 
 constexpr long long kHostChunkMin = 1LL << 18;   // points per pipelined chunk of qed_eval_msq_host (minimum)
 
-// QED_HOST_ONSHELL (include/qed.h): restore the energy rows of one uploaded chunk from the mass shell,
-// E_j = sqrt(|p_j|^2 + m_j^2), m = 1 for the particles in electron_mask (bit j), 0 for the photons.
-// One thread per (point, particle), consecutive threads on consecutive points: coalesced 8-byte rows.
+// QED_HOST_ONSHELL / QED_HOST_CONSERVE (include/qed.h): complete one uploaded chunk.  One thread per point
+// (consecutive threads on consecutive points: coalesced 8-byte rows).  CONSERVE: the outgoing electron's
+// 3-momentum p' = p + sum_in k - sum_out k (rows of particle e_out were not uploaded); then every energy row
+// E_j = sqrt(|p_j|^2 + m_j^2), m = 1 for the two electrons, 0 for the photons.
 __global__ void __launch_bounds__(256) qed_onshell_energy_kernel(double* __restrict__ mom, long long cnt, int n_ext,
-                                                                 unsigned electron_mask) {
-  const long long total = cnt * n_ext;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(t / cnt);
-    const long long i = t - (long long)j * cnt;
-    double* r = mom + (long long)(4 * j) * cnt + i;
-    const double px = r[cnt], py = r[2 * cnt], pz = r[3 * cnt];
-    const double m2 = ((electron_mask >> j) & 1u) ? 1.0 : 0.0;
-    r[0] = sqrt(fma(px, px, fma(py, py, fma(pz, pz, m2))));
+                                                                 int e_out, int conserve) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
+    double* r = mom + i;
+    if (conserve) {
+      double px = 0.0, py = 0.0, pz = 0.0;
+      for (int j = 0; j < n_ext; ++j) {
+        if (j == e_out) continue;
+        const double sg = j < e_out ? 1.0 : -1.0;   // incoming: e- and photons before e_out
+        px = fma(sg, r[(4 * j + 1) * cnt], px);
+        py = fma(sg, r[(4 * j + 2) * cnt], py);
+        pz = fma(sg, r[(4 * j + 3) * cnt], pz);
+      }
+      r[(4 * e_out + 1) * cnt] = px;
+      r[(4 * e_out + 2) * cnt] = py;
+      r[(4 * e_out + 3) * cnt] = pz;
+    }
+    for (int j = 0; j < n_ext; ++j) {
+      const double px = r[(4 * j + 1) * cnt], py = r[(4 * j + 2) * cnt], pz = r[(4 * j + 3) * cnt];
+      const double m2 = (j == 0 || j == e_out) ? 1.0 : 0.0;
+      r[4 * j * cnt] = sqrt(fma(px, px, fma(py, py, fma(pz, pz, m2))));
+    }
   }
 }
 
@@ -418,8 +431,12 @@ qed_status qed_eval_msq_host_ex(const qed_process* cproc, const double* momenta_
                                 double* out_host, uint32_t flags) {
   qed_process* P = const_cast<qed_process*>(cproc);
   if (!P) return fail(QED_ERR_INVALID_ARGUMENT, "proc is NULL");
-  if (flags & ~QED_HOST_ONSHELL) return fail(QED_ERR_INVALID_ARGUMENT, "unknown flag bits in qed_eval_msq_host_ex");
-  const bool onshell = (flags & QED_HOST_ONSHELL) != 0;
+  if (flags & ~(QED_HOST_ONSHELL | QED_HOST_CONSERVE))
+    return fail(QED_ERR_INVALID_ARGUMENT, "unknown flag bits in qed_eval_msq_host_ex");
+  if ((flags & QED_HOST_CONSERVE) && !(flags & QED_HOST_ONSHELL))
+    return fail(QED_ERR_INVALID_ARGUMENT, "QED_HOST_CONSERVE requires QED_HOST_ONSHELL");
+  const bool onshell = (flags & QED_HOST_ONSHELL) != 0, conserve = (flags & QED_HOST_CONSERVE) != 0;
+  const int e_out = P->args.e_out_particle;
   if (n_points < 0) return fail(QED_ERR_INVALID_ARGUMENT, "n_points < 0");
   if (n_points == 0) return QED_OK;
   if (!momenta_host || !out_host) return fail(QED_ERR_INVALID_ARGUMENT, "momenta/out is NULL");
@@ -471,6 +488,7 @@ qed_status qed_eval_msq_host_ex(const qed_process* cproc, const double* momenta_
     const int nblk = onshell ? P->n_ext : 1, blk_rows = onshell ? 3 : rows;
     e = cudaSuccess;
     for (int k = 0; k < nblk && e == cudaSuccess; ++k) {
+      if (conserve && k == e_out) continue;   // p' follows from momentum conservation on the device
       const int r0 = onshell ? 4 * k + 1 : 0;
       if (spitch <= (size_t)max_pitch) {
         e = cudaMemcpy2DAsync(P->d_mom[b] + (size_t)r0 * cnt, sizeof(double) * (size_t)cnt,
@@ -484,10 +502,8 @@ qed_status qed_eval_msq_host_ex(const qed_process* cproc, const double* momenta_
     }
     if (e != cudaSuccess) return drain(cuda_fail(e, "H2D copy"));
     if (onshell) {
-      const unsigned emask = 1u | (1u << P->args.e_out_particle);
-      const long long work = cnt * P->n_ext;
-      const int grid = (int)std::min<long long>((work + 255) / 256, 8LL * P->num_sms);
-      qed_onshell_energy_kernel<<<grid, 256, 0, st>>>(P->d_mom[b], cnt, P->n_ext, emask);
+      const int grid = (int)std::min<long long>((cnt + 255) / 256, 8LL * P->num_sms);
+      qed_onshell_energy_kernel<<<grid, 256, 0, st>>>(P->d_mom[b], cnt, P->n_ext, e_out, conserve ? 1 : 0);
       e = cudaGetLastError();
       if (e != cudaSuccess) return drain(cuda_fail(e, "on-shell energy kernel launch"));
       g_launches.fetch_add(1);

@@ -17,6 +17,7 @@ QED_OK = 0
 QED_SUM = -1
 MC_CHUNK = 1024
 HOST_ONSHELL = 1   # QED_HOST_ONSHELL (include/qed.h)
+HOST_CONSERVE = 2  # QED_HOST_CONSERVE (include/qed.h)
 _STATUS = {0: "QED_OK", 1: "QED_ERR_INVALID_ARGUMENT", 2: "QED_ERR_UNSUPPORTED", 3: "QED_ERR_CUDA",
            4: "QED_ERR_OUT_OF_MEMORY", 5: "QED_ERR_INTERNAL"}
 
@@ -218,15 +219,18 @@ class Process:
                                          _ptr(out, n_points * H, "out", self.device), _stream_ptr(stream)),
                "qed_eval_msq_configs")
 
-    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int | None = None, onshell: bool = False) -> None:
+    def eval_msq_host(self, momenta_soa_host, out_host, n_points: int | None = None, onshell: bool = False,
+                      conserve: bool = False) -> None:
         """Host buffers (pinned recommended): momenta [(4*n_ext), n_points], out [n_points].
         onshell=True: qed_eval_msq_host_ex(QED_HOST_ONSHELL), only the 3-momenta are uploaded and the
-        energies are restored on the device from the mass shell (include/qed.h)."""
+        energies are restored on the device from the mass shell; conserve=True (with onshell) adds
+        QED_HOST_CONSERVE, the outgoing electron is restored from momentum conservation (include/qed.h)."""
         n_points = out_host.numel() if n_points is None else n_points
         mom = self._soa(momenta_soa_host, n_points, None)
         out = _ptr(out_host, n_points, "out", None)
-        if onshell:
-            _check(_lib.qed_eval_msq_host_ex(self._h, mom, n_points, out, HOST_ONSHELL), "qed_eval_msq_host_ex")
+        if onshell or conserve:
+            flags = (HOST_ONSHELL if onshell else 0) | (HOST_CONSERVE if conserve else 0)
+            _check(_lib.qed_eval_msq_host_ex(self._h, mom, n_points, out, flags), "qed_eval_msq_host_ex")
         else:
             _check(_lib.qed_eval_msq_host(self._h, mom, n_points, out), "qed_eval_msq_host")
 

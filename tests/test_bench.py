@@ -46,7 +46,10 @@ def test_b200_arm_json_one_and_two_ranks():
     assert KEYS <= set(d1) and d1["n_gpus"] == 1 and d1["value"] > 0
     r = d1["roofline"]
     assert r["bound"] == "alu" and 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
-    assert d1["e2e"]["h2d_bytes_per_step"] == 262144 * 4 * 4 * 8 and d1["e2e"]["d2h_bytes_per_step"] == 262144 * 8
+    # ONSHELL | CONSERVE: the 3 momentum rows of 3 of the 4 particles cross PCIe; full_4momenta all 16 rows
+    assert d1["e2e"]["h2d_bytes_per_step"] == 262144 * 3 * 3 * 8 and d1["e2e"]["d2h_bytes_per_step"] == 262144 * 8
+    assert d1["e2e"]["onshell_3momenta"]["h2d_bytes_per_step"] == 262144 * 4 * 3 * 8
+    assert d1["e2e"]["full_4momenta"]["h2d_bytes_per_step"] == 262144 * 4 * 4 * 8 and d1["e2e"]["full_4momenta"]["value"] > 0
     assert d1["gpu_launches"] >= 3 and "sm_mhz" in d1["clocks"]
     assert d1["clocks"]["samples"] >= 3, d1["clocks"]          # NVML polling covers the short timed region
     for key, n, total in (("c3_strong", 3, (1 << 24) >> 6), ("c5_strong", 5, (1 << 26) >> 6)):

@@ -243,12 +243,14 @@ def test_host_entry_point_pipelined_chunks(qed):
     assert torch.equal(out2, out)
 
 
+@pytest.mark.parametrize("conserve", [False, True])
 @pytest.mark.parametrize("n,n_in,algorithm", [(2, 1, "cdag"), (3, 3, "bg")])
-def test_host_entry_point_onshell(qed, n, n_in, algorithm):
-    """qed_eval_msq_host_ex(QED_HOST_ONSHELL): only the 3-momenta are uploaded and the energies are
-    restored on the device from the mass shell (include/qed.h).  The host energy rows are poisoned with
-    NaN to prove they are not read; oracle on the original momenta, over pipelined chunks with a
-    ragged tail, in the north-star and the paper direction (electron rows 0 and n_in + 1)."""
+def test_host_entry_point_onshell(qed, n, n_in, algorithm, conserve):
+    """qed_eval_msq_host_ex(QED_HOST_ONSHELL [| QED_HOST_CONSERVE]): only the 3-momenta are uploaded and
+    the energies are restored on the device from the mass shell; with CONSERVE the outgoing electron's
+    rows are not uploaded either and follow from momentum conservation (include/qed.h).  The rows that
+    must not be read are poisoned with NaN on the host; oracle on the original momenta, over pipelined
+    chunks with a ragged tail, in the north-star and the paper direction (electron rows 0 and n_in + 1)."""
     P = 2 * (1 << 18) + 777
     mom = synthetic.rambo_cm(n if n_in == 1 else n, P, sqrt_s=5.0, seed=8200 + n).numpy()
     if n_in > 1:   # time-reversed north-star kinematics (test_paper_direction_matches_oracle)
@@ -260,8 +262,10 @@ def test_host_entry_point_onshell(qed, n, n_in, algorithm):
     torch.cuda.synchronize()
     poisoned = soa.clone()
     poisoned[0::4] = float("nan")
+    if conserve:
+        poisoned[4 * (n_in + 1):4 * (n_in + 2)] = float("nan")
     out = torch.full((P,), float("nan"), dtype=torch.float64).pin_memory()
-    proc.eval_msq_host(poisoned.pin_memory(), out, P, onshell=True)
+    proc.eval_msq_host(poisoned.pin_memory(), out, P, onshell=True, conserve=conserve)
     got = out.numpy()
     assert np.all(np.isfinite(got))
     # same points as the device path up to the rounding of the given energies, amplified by the
@@ -273,8 +277,9 @@ def test_host_entry_point_onshell(qed, n, n_in, algorithm):
                                     worst]))
     ref = oracle.msq(n_in, n + 1 - n_in, mom[idx])
     assert np.max(np.abs(got[idx] / ref - 1)) <= TOL
-    with pytest.raises(qed.QedError):
-        qed._check(qed._lib.qed_eval_msq_host_ex(proc._h, poisoned.data_ptr(), P, out.data_ptr(), 2), "flags")
+    for bad in (2, 4):   # CONSERVE without ONSHELL; an unknown bit
+        with pytest.raises(qed.QedError):
+            qed._check(qed._lib.qed_eval_msq_host_ex(proc._h, poisoned.data_ptr(), P, out.data_ptr(), bad), "flags")
 
 
 def test_two_streams_two_handles(qed):
