@@ -34,6 +34,9 @@ for algo, n, npts in cases:
     if n <= 2:   # host entry point (pinned staging, two streams)
         hout = torch.empty(npts, dtype=torch.float64).pin_memory()
         proc.eval_msq_host(soa.cpu().pin_memory(), hout, npts)
+        # 3-momentum uploads with the on-shell / conservation completion kernel (qed_eval_msq_host_ex)
+        proc.eval_msq_host(soa.cpu().pin_memory(), hout, npts, onshell=True)
+        proc.eval_msq_host(soa.cpu().pin_memory(), hout, npts, onshell=True, conserve=True)
     torch.cuda.synchronize()
     assert torch.isfinite(out).all(), (algo, n)
     print(algo, n, "ok", flush=True)
