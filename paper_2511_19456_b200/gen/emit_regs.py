@@ -392,8 +392,9 @@ def emit_regs_body_bg(N: int = 3) -> str:
         for lb in range(2):
             w(f"      {{ __syncwarp();  // scheduling fence: keeps ptxas from hoisting every J_in load")
             w(f"        qed::spinor K0 = qed::eslash_row(e[{c}][0], P[{b}][{lb}]), K1 = qed::eslash_row_t(e[{c}][1], P[{b}][{lb}]);")
-            w(f"        qed::add_to(K0, qed::eslash_row{T_[lb]}(e[{b}][{lb}], P[{c}][0]));")
-            w(f"        qed::add_to(K1, qed::eslash_row{T_[lb]}(e[{b}][{lb}], P[{c}][1]));")
+            # accumulating vertex (3 DFMA per output, no DMUL + DADD): same 48-flop model, 8 fewer pipe slots
+            w(f"        qed::eslash_row{T_[lb]}_acc(e[{b}][{lb}], P[{c}][0], K0);")
+            w(f"        qed::eslash_row{T_[lb]}_acc(e[{b}][{lb}], P[{c}][1], K1);")
             w("        #pragma unroll")
             w("        for (int k = 0; k < 4; ++k) {")
             w(f"          const qed::spinor ph = qed::ld_spinor_stream(sl + ({a_} * 4 + k) * 8);")
@@ -626,8 +627,10 @@ struct T1 {{
     bg_c = ""
     if N == 3:
         # Berends-Giele variants; r32 sweep: 2.91e9 pts/s without the L2 prefetch, 2.81e9 with it
-        # (r44: moving the complement propagator constants to the private slot, at 7 warps/SM, measured -12 %)
-        bvs = [("T1B", 8, 1, 0), ("T1B", 8, 1, 1), ("T1B", 4, 2, 1)]
+        # (r44: moving the complement propagator constants to the private slot, at 7 warps/SM, measured -12 %).
+        # Session-3 A/B (profiles/ab_s3_t1b.jsonl): with the accumulating K_out vertices the L2 prefetch
+        # variant is 1.9 % ahead (3.11e9 vs 3.06e9) -> first
+        bvs = [("T1B", 8, 1, 1), ("T1B", 8, 1, 0), ("T1B", 4, 2, 1)]
         variant_structs += "".join(
             f"struct B{i} {{ static constexpr int WPB = {w_}, MIN_BLOCKS = {m}, PF = {p_}; }};\n" for i, (d, w_, m, p_) in enumerate(bvs))
         bcases = "\n".join(
