@@ -245,6 +245,22 @@ def traffic_from_profile(n: int, points: int):
         return None
 
 
+def generic_flops(n: int, algorithm: str, flops: int) -> int:
+    """Flops per point of the register kernels (n <= 2) under the generic per-node model (every vertex 40 / 24,
+    every propagator 56 flop, as for the lane-group kernels), i.e. without the skipped structural zeros of the
+    external spinors (gen/emit_regs.py sparse_*); other kernels: their own count."""
+    if n > 2:
+        return flops
+    from paper_2511_19456_b200.gen import emit_regs as er
+    gv = {False: 40 + 56, True: 24 + 56}
+    extra_u = sum(gv[lam == 1] - er.sparse_vs(er.ZU[s], lam == 1) for s in range(2) for lam in range(2))
+    if n == 1:
+        extra_ub = sum({False: 40, True: 24}[lam == 1] - er.sparse_v(er.ZU[s], lam == 1)[0] for s in range(2) for lam in range(2))
+        return flops + 2 * extra_u + 2 * extra_ub
+    extra_ub = sum(gv[lam == 1] - er.sparse_vs(er.ZUX, lam == 1) for lam in range(2))
+    return flops + 3 * extra_u + 3 * 2 * extra_ub
+
+
 def l1_roofline(algorithm: str, n: int, points: int, seconds: float):
     """Second roofline for the lane-group Berends-Giele kernels, which are bound by the L1 data pipe (shared +
     global LSU wavefronts, 1 per clock per SM; DESIGN.md §6 kernel 2b) rather than by FP64: wavefronts per
@@ -590,6 +606,13 @@ def run_b200(args, world, rank, local):
                 "algorithmic_bytes_per_point": info["bytes_per_point"],
                 "hbm_gbs": round(info["bytes_per_point"] * P / kernel_s / 1e9, 1),
                 "peak_note": "FP64 CUDA-core peak 148 SM x 128 flop/clk x 1965 MHz (DESIGN.md Roofline)"}
+    gen_fl = generic_flops(n, args.algorithm, info["flops_per_point"])
+    if gen_fl != info["flops_per_point"]:
+        # the register kernels skip the structural zeros of u / ubar (csrc/qed_sparse.cuh) and count only the
+        # products they need; the per-node model of the lane-group kernels and of round 1 (V 40 / 24, S 56 on
+        # every node) is kept beside it for comparison
+        roofline["generic_model_flops_per_point"] = gen_fl
+        roofline["frac_generic_model"] = round(gen_fl * P / kernel_s / 1e12 / FP64_PEAK_TFLOPS, 4)
     if clk.get("sm_mhz"):
         roofline["frac_at_observed_clock"] = round(
             achieved / (148 * 128 * clk["sm_mhz"] * 1e6 / 1e12), 4)

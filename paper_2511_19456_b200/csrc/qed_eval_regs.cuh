@@ -8,6 +8,7 @@
 // where the group kernel (qed_eval_kernel.cuh) is bound by shared-memory traffic.
 #pragma once
 #include "qed_device.cuh"
+#include "qed_sparse.cuh"
 #include "qed_kernel_args.h"
 
 namespace qed {

@@ -27,7 +27,8 @@ from .lower import FLOPS
 
 def _flops(N: int) -> dict:
     """Flops per point of the emitted body.  Half of every vertex count has lam = 1, whose
-    polarisation eps(k, 2) is transverse (eps^3 = 0): V_T = 24 instead of V = 40."""
+    polarisation eps(k, 2) is transverse (eps^3 = 0): V_T = 24 instead of V = 40; vertices and propagators
+    applied to the external spinors skip those spinors' structural zeros (sparse_v / sparse_s)."""
     H = 1 << (N + 2)
     n_phi = N * 4                                   # leaves phi_a[s][lam]
     if N == 2:
@@ -37,11 +38,21 @@ def _flops(N: int) -> dict:
         n_leaf = N * (N - 1) * 4 * 2                # (b, c) x lam_b lam_c x s'
     import math
     V2 = FLOPS["V"] + FLOPS["V_T"]                  # one vertex of each polarisation
+    # vertices on the external spinors skip their structural zeros (qed_sparse.cuh): the phi leaves on
+    # u(p, s) with s known at build time; the out-side first level on ubar(p', s'): known at n = 1 (both s'
+    # in one body), a run-time pass variable at n = 2 (ZUX)
+    vs_u = sum(sparse_vs(ZU[s_], lam == 1) for s_ in range(2) for lam in range(2))          # one photon
+    if N == 2:
+        v_ub = sum(sparse_v(ZU[s_], lam == 1)[0] for s_ in range(2) for lam in range(2))   # one photon
+        trie_out = N * v_ub
+    else:
+        vs_ub = sum(sparse_vs(ZUX, lam == 1) for lam in range(2))                           # one photon, one s'
+        trie_out = N * 2 * vs_ub + n_leaf // 2 * V2
     return {
         "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
         "propagator_constants": (N + (N if N > 2 else 0)) * FLOPS["MASK"],
-        "trie_in": n_phi // 2 * V2 + n_phi * FLOPS["S"],
-        "trie_out": n_int // 2 * V2 + n_int * FLOPS["S"] + n_leaf // 2 * V2,
+        "trie_in": N * vs_u,
+        "trie_out": trie_out,
         "join": math.factorial(N) * H * FLOPS["JOIN"],
         "msq": H * FLOPS["ABS2"],
     }
@@ -63,6 +74,51 @@ def slot_layout(N: int) -> dict:
 
 
 T_ = ("", "_t")   # vertex of polarisation lam: eps(k, 2) (lam = 1) is transverse, eps^3 = 0
+
+# Structural zeros of the external spinors (csrc/qed_sparse.cuh ZU0 / ZU1 / ZUX; bit 2c + j = component c,
+# j = 0 real / 1 imaginary): u(p, 0) = ubar-pattern(p', 0) = (n, 0, ., 0 + ...), u(p, 1) likewise; ZUX = both
+# (spin chosen at run time).  The register bodies skip the products with them (qed_sparse.cuh).
+ZU = (0b00101110, 0b10001011)
+ZUX = ZU[0] & ZU[1]
+
+
+def _zb(Z: int, k: int) -> bool:
+    return bool((Z >> k) & 1)
+
+
+def _cnt(zero_flags) -> int:
+    """flops of one real output that sums the non-zero products among its terms: 1 DMUL + (k - 1) DFMA."""
+    k = sum(1 for z in zero_flags if not z)
+    return 2 * k - 1 if k else 0
+
+
+def sparse_v(Z: int, T: bool) -> tuple[int, int]:
+    """(flops, output zero pattern) of the vertex epsslash psi / psibar epsslash on input pattern Z, mirroring
+    qed_sparse.cuh emul_col_z / emul_row_z; T: transverse eps (e3 = 0).  Z = 0 gives the generic 40 / 24."""
+    fl, zout = 0, 0
+    for oc, (xc, yc) in ((0, (2, 3)), (2, (0, 1))):
+        xr, xi, yr, yi = _zb(Z, 2 * xc), _zb(Z, 2 * xc + 1), _zb(Z, 2 * yc), _zb(Z, 2 * yc + 1)
+        outs = [[T or xr, yr, yi], [T or xi, yi, yr], [xr, xi, T or yr], [xi, xr, T or yi]]
+        for k, terms in enumerate(outs):
+            fl += _cnt(terms)
+            if all(terms):
+                zout |= 1 << (2 * oc + k)
+    return fl, zout
+
+
+def sparse_s(Z: int) -> int:
+    """flops of the propagator (Qslash + m)/D on input pattern Z (qed_sparse.cuh prop_col_z / prop_row_z, same
+    term structure); Z = 0 gives the generic 56."""
+    z = [_zb(Z, k) for k in range(8)]
+    outs = [[z[0], z[4], z[6], z[7]], [z[1], z[5], z[7], z[6]], [z[2], z[4], z[5], z[6]], [z[3], z[5], z[4], z[7]],
+            [z[4], z[0], z[2], z[3]], [z[5], z[1], z[3], z[2]], [z[6], z[0], z[1], z[2]], [z[7], z[1], z[0], z[3]]]
+    return sum(_cnt(t) for t in outs)
+
+
+def sparse_vs(Z: int, T: bool) -> int:
+    """V then S on an external spinor with zero pattern Z (qed_sparse.cuh vs_col_z / vs_row_z)."""
+    fv, zv = sparse_v(Z, T)
+    return fv + sparse_s(zv)
 
 
 def emit_regs_body(N: int) -> str:
@@ -195,11 +251,11 @@ def emit_regs_body1(N: int) -> str:
         w(f"  {{  // in-side photon {a_}: phi[s][lam_{a_}] = S(Q_{a_}) epsslash u(p, s); out-side leaves ubar(s') epsslash_{b}")
         w("    qed::spinor ph[2][2];")
         for s, us in ((0, "u0"), (1, "u1")):
-            w(f"    ph[{s}][0] = qed::prop_col(m[{a_}], qed::eslash_col(e[{a_}][0], {us}));")
-            w(f"    ph[{s}][1] = qed::prop_col(m[{a_}], qed::eslash_col_t(e[{a_}][1], {us}));")
+            w(f"    ph[{s}][0] = qed::vs_col_z<qed::ZU{s}, false>(m[{a_}], e[{a_}][0], {us});")
+            w(f"    ph[{s}][1] = qed::vs_col_z<qed::ZU{s}, true>(m[{a_}], e[{a_}][1], {us});")
         for lb in range(2):
             for sp, ubs in ((0, "ub0"), (1, "ub1")):
-                w(f"    {{ const qed::spinor leaf = qed::eslash_row{T_[lb]}(e[{b}][{lb}], {ubs});")
+                w(f"    {{ const qed::spinor leaf = qed::eslash_row_z<qed::ZU{sp}, {'true' if lb else 'false'}>(e[{b}][{lb}], {ubs});")
                 for s in range(2):
                     for la in range(2):
                         idx = s | (la << (1 + a_)) | (lb << (1 + b)) | (sp << 3)
@@ -251,7 +307,7 @@ def emit_regs_body1p(N: int, fence: bool = True, inter: bool = False) -> str:
         w(f"    {{ double m[5]; qed::mask_regs(pe, q[{a_}], sg[{a_}], m);")
         for s_, us in ((0, "u0"), (1, "u1")):
             for lam in range(2):
-                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::prop_col(m, qed::eslash_col{T_[lam]}(e[{a_}][{lam}], {us})));")
+                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::vs_col_z<qed::ZU{s_}, {'true' if lam else 'false'}>(m, e[{a_}][{lam}], {us}));")
         w("    }")
     w("  }")
     w("  // propagator constants of S(Q_{all \\ b}): Q = p + sum_{i != b} sg_i k_i")
@@ -270,10 +326,13 @@ def emit_regs_body1p(N: int, fence: bool = True, inter: bool = False) -> str:
     w("    #pragma unroll")
     w("    for (int i = 0; i < 32; ++i) acc[i] = 0.0;")
     w("    const qed::spinor ub = qed::ubar_spinor(pp, sp);")
+    # s' is the run-time pass index: ubar(p', s') with the zeros common to both spins (ZUX); instantiating
+    # the two passes separately for the full pattern measured 5-10 % slower (code size, sweep_s3_unroll_rejected)
+    zub = "qed::ZUX"
     for b in range(3):
         for lb in range(2):
             w(f"    {{  // tau_1 = photon {b}, lam_{b} = {lb}")
-            w(f"      const qed::spinor I = qed::prop_row(mc[{b}], qed::eslash_row{T_[lb]}(e[{b}][{lb}], ub));")
+            w(f"      const qed::spinor I = qed::vs_row_z<{zub}, {'true' if lb else 'false'}>(mc[{b}], e[{b}][{lb}], ub);")
             for c in range(3):
                 if c == b:
                     continue
@@ -317,8 +376,8 @@ def bg_flops(N: int = 3) -> dict:
     return {
         "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
         "propagator_constants": 2 * N * FLOPS["MASK"],
-        "currents_in": 6 * V2 + 12 * FLOPS["S"],            # J_in({a})[s][lam]
-        "currents_out": 6 * V2 + 12 * FLOPS["S"],           # P_out({b})[s'][lam]
+        "currents_in": N * sum(sparse_vs(ZU[s_], lam == 1) for s_ in range(2) for lam in range(2)),  # J_in({a})[s][lam]
+        "currents_out": N * 2 * sum(sparse_vs(ZUX, lam == 1) for lam in range(2)),   # P_out({b})[s'][lam], s' per pass
         "k_sums": 2 * 3 * (2 * 2 * V2 + 4 * 8),             # K_out(A^c)[s'][lam_b][lam_c]
         "join": 2 * 3 * 4 * 4 * FLOPS["JOIN"],              # one join per subset {a} and configuration
         "msq": H * FLOPS["ABS2"],
@@ -363,7 +422,7 @@ def emit_regs_body_bg(N: int = 3) -> str:
         w(f"    {{ double m[5]; qed::mask_regs(pe, q[{a_}], sg[{a_}], m);")
         for s_, us in ((0, "u0"), (1, "u1")):
             for lam in range(2):
-                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::prop_col(m, qed::eslash_col{T_[lam]}(e[{a_}][{lam}], {us})));")
+                w(f"      qed::st_spinor(sl + {(a_ * 4 + s_ * 2 + lam) * 8}, qed::vs_col_z<qed::ZU{s_}, {'true' if lam else 'false'}>(m, e[{a_}][{lam}], {us}));")
         w("    }")
     w("  }")
     w("  double mc[3][5];   // S(Q_{all \\ x})")
@@ -385,7 +444,7 @@ def emit_regs_body_bg(N: int = 3) -> str:
 
     def pout(x):
         for lam in range(2):
-            w(f"    P[{x}][{lam}] = qed::prop_row(mc[{x}], qed::eslash_row{T_[lam]}(e[{x}][{lam}], ub));")
+            w(f"    P[{x}][{lam}] = qed::vs_row_z<qed::ZUX, {'true' if lam else 'false'}>(mc[{x}], e[{x}][{lam}], ub);")
 
     def block(a_, b, c):
         w(f"    {{  // subset {{{a_}}}: K_out({{{b}, {c}}}) . J_in({{{a_}}})")

@@ -193,7 +193,22 @@ def test_bg_join_halves_match_oracle(N, hs):
 
 # ---------------------------------------------------------------- register bodies: flop counts from the emitted code
 _CALL_FLOPS = {"eslash_col(": 40, "eslash_row(": 40, "eslash_col_t(": 24, "eslash_row_t(": 24, "prop_col(": 56,
-               "prop_row(": 56, "cdot_acc(": 32, "cdot8_acc(": 8 * 32, "add_to(": 8}
+               "prop_row(": 56, "cdot_acc(": 32, "cdot8_acc(": 8 * 32, "add_to(": 8,
+               "eslash_row_acc(": 48, "eslash_row_t_acc(": 32}
+
+
+def _sparse_call_flops():
+    """qed_sparse.cuh calls on the external spinors, priced by the generator's zero-aware count."""
+    from paper_2511_19456_b200.gen.emit_regs import ZU, ZUX, sparse_v, sparse_vs
+    out = {}
+    for zn, z in (("ZU0", ZU[0]), ("ZU1", ZU[1]), ("ZUX", ZUX)):
+        for t in (False, True):
+            tn = "true" if t else "false"
+            out[f"vs_col_z<qed::{zn}, {tn}>("] = sparse_vs(z, t)
+            out[f"vs_row_z<qed::{zn}, {tn}>("] = sparse_vs(z, t)
+            out[f"eslash_row_z<qed::{zn}, {tn}>("] = sparse_v(z, t)[0]
+            out[f"eslash_col_z<qed::{zn}, {tn}>("] = sparse_v(z, t)[0]
+    return out
 
 
 def _count_body_flops(src: str, fn: str) -> int:
@@ -210,7 +225,7 @@ def _count_body_flops(src: str, fn: str) -> int:
             mult *= k
         if m:
             pending = int(m.group(1))
-        for call, fl in _CALL_FLOPS.items():
+        for call, fl in {**_CALL_FLOPS, **_sparse_call_flops()}.items():
             total += mult * (pending if m else 1) * fl * line.count(call)
         for ch in line:
             if ch == "{":
@@ -232,11 +247,38 @@ def test_register_body_flops_match_the_flop_model():
         vertex_part = sum(v for k, v in model.items() if k not in ("external", "propagator_constants", "msq"))
         got = _count_body_flops(src, fn)
         if fn == "regs_body_bg_N3":
-            got -= 2 * (40 + 24 + 2 * 56)      # P_out({1}) recomputed once per s' pass
+            from paper_2511_19456_b200.gen.emit_regs import ZUX, sparse_vs
+            got -= 2 * (sparse_vs(ZUX, False) + sparse_vs(ZUX, True))   # P_out({1}) recomputed once per s' pass
         assert got == vertex_part, (fn, got, vertex_part)
     # the generic plan minus the transverse-vertex saving (16 flop per eps(k, 2) vertex, half of all vertices)
-    assert sum(_flops(2).values()) == make_plan(2).flops_per_point - 16 * 8
-    assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36
+    # and minus the structural zeros of u / ubar skipped by the vertices and propagators on them
+    from paper_2511_19456_b200.gen.emit_regs import ZU, ZUX, sparse_vs, sparse_v
+    gen_vs = {False: 40 + 56, True: 24 + 56}
+    save_u = sum(gen_vs[lam == 1] - sparse_vs(ZU[s], lam == 1) for s in range(2) for lam in range(2))
+    save_ub1 = sum({False: 40, True: 24}[lam == 1] - sparse_v(ZU[s], lam == 1)[0] for s in range(2) for lam in range(2))
+    save_ubx = sum(gen_vs[lam == 1] - sparse_vs(ZUX, lam == 1) for lam in range(2))
+    assert sum(_flops(2).values()) == make_plan(2).flops_per_point - 16 * 8 - 2 * save_u - 2 * save_ub1
+    assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36 - 3 * save_u - 3 * 2 * save_ubx
+
+
+def test_sparse_external_patterns_and_generic_counts():
+    """The structural zero patterns the register kernels skip (qed_sparse.cuh ZU0 / ZU1, gen ZU) are exactly the
+    zeros of the oracle's u(p, s) and ubar(p, s) at generic momenta, and the zero-aware counts reduce to the
+    generic flop model (V 40, V_T 24, S 56) on a spinor without zeros."""
+    from paper_2511_19456_b200.gen.emit_regs import ZU, ZUX, sparse_s, sparse_v
+    rng = np.random.default_rng(5)
+    for _ in range(5):
+        pv = rng.normal(size=3)
+        p = np.array([np.sqrt(1.0 + pv @ pv), *pv])
+        for s in range(2):
+            for sp in (oracle.spinor_u(p, s), oracle.spinor_ubar(p, s)):
+                re_im = np.stack([sp.real, sp.imag], axis=1).reshape(-1)   # bit 2c + j
+                z = sum(1 << k for k in range(8) if re_im[k] == 0.0)
+                assert z == ZU[s], (s, bin(z))
+    assert ZUX == ZU[0] & ZU[1]
+    assert sparse_v(0, False) == (40, 0) and sparse_v(0, True) == (24, 0) and sparse_s(0) == 56
+    # a zero input component removes exactly the products it enters (each appears in 3 of the 8 V outputs)
+    assert sparse_v(1, False)[0] == 40 - 2 * 3
 
 
 # ---------------------------------------------------------------- grouped Berends-Giele tasks (round 3)
