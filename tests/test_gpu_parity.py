@@ -280,6 +280,15 @@ def test_host_entry_point_onshell(qed, n, n_in, algorithm, conserve):
     for bad in (2, 4):   # CONSERVE without ONSHELL; an unknown bit
         with pytest.raises(qed.QedError):
             qed._check(qed._lib.qed_eval_msq_host_ex(proc._h, poisoned.data_ptr(), P, out.data_ptr(), bad), "flags")
+    # a tiny call (one partial chunk, one block of the completion kernel) and an empty one
+    small = synthetic.to_soa(torch.from_numpy(mom[:5]))
+    small[0::4] = float("nan")
+    if conserve:
+        small[4 * (n_in + 1):4 * (n_in + 2)] = float("nan")
+    out5 = torch.full((5,), float("nan"), dtype=torch.float64)
+    proc.eval_msq_host(small, out5, 5, onshell=True, conserve=conserve)
+    assert np.max(np.abs(out5.numpy() / oracle.msq(n_in, n + 1 - n_in, mom[:5]) - 1)) <= TOL
+    proc.eval_msq_host(small[:, :0].contiguous(), out5[:0], 0, onshell=True, conserve=conserve)
 
 
 def test_two_streams_two_handles(qed):
