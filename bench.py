@@ -257,8 +257,11 @@ def generic_flops(n: int, algorithm: str, flops: int) -> int:
     if n == 1:
         extra_ub = sum({False: 40, True: 24}[lam == 1] - er.sparse_v(er.ZU[s], lam == 1)[0] for s in range(2) for lam in range(2))
         return flops + 2 * extra_u + 2 * extra_ub
-    extra_ub = sum(gv[lam == 1] - er.sparse_vs(er.ZUX, lam == 1) for lam in range(2))
-    return flops + 3 * extra_u + 3 * 2 * extra_ub
+    if algorithm == "bg":   # P_out on ubar with the zeros common to both s' (ZUX)
+        extra_ub = 2 * sum(gv[lam == 1] - er.sparse_vs(er.ZUX, lam == 1) for lam in range(2))
+    else:                   # CDAG: the per-spin specialisation (vs_row_ub)
+        extra_ub = sum(gv[lam == 1] - er.sparse_vs(er.ZU[s], lam == 1) for s in range(2) for lam in range(2))
+    return flops + 3 * extra_u + 3 * extra_ub
 
 
 def l1_roofline(algorithm: str, n: int, points: int, seconds: float):

@@ -149,4 +149,17 @@ __device__ __forceinline__ spinor vs_row_z(const double* mk, const double* e, co
   return prop_row_z<z_eslash(Z, T)>(mk, eslash_row_z<Z, T>(e, ub));
 }
 
+// ubar(p', s') epsslash S(Q) with s' a warp-uniform run-time value (the register kernels' pass index): one
+// specialisation per spin behind a uniform branch, so each pass skips all four zeros of its ubar
+template <bool T>
+__device__ __forceinline__ spinor vs_row_ub(const double* mk, const double* e, const spinor& ub, int sp) {
+  spinor o;
+  if (sp == 0) {
+    o = vs_row_z<ZU0, T>(mk, e, ub);
+  } else {
+    o = vs_row_z<ZU1, T>(mk, e, ub);
+  }
+  return o;
+}
+
 }  // namespace qed

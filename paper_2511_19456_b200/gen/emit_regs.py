@@ -39,15 +39,15 @@ def _flops(N: int) -> dict:
     import math
     V2 = FLOPS["V"] + FLOPS["V_T"]                  # one vertex of each polarisation
     # vertices on the external spinors skip their structural zeros (qed_sparse.cuh): the phi leaves on
-    # u(p, s) with s known at build time; the out-side first level on ubar(p', s'): known at n = 1 (both s'
-    # in one body), a run-time pass variable at n = 2 (ZUX)
+    # u(p, s) and the out-side first level on ubar(p', s'), s and s' known at build time (n = 1) or selected per
+    # pass by a uniform branch (n = 2, vs_row_ub)
     vs_u = sum(sparse_vs(ZU[s_], lam == 1) for s_ in range(2) for lam in range(2))          # one photon
     if N == 2:
         v_ub = sum(sparse_v(ZU[s_], lam == 1)[0] for s_ in range(2) for lam in range(2))   # one photon
         trie_out = N * v_ub
     else:
-        vs_ub = sum(sparse_vs(ZUX, lam == 1) for lam in range(2))                           # one photon, one s'
-        trie_out = N * 2 * vs_ub + n_leaf // 2 * V2
+        vs_ub = sum(sparse_vs(ZU[s_], lam == 1) for s_ in range(2) for lam in range(2))   # one photon, both s'
+        trie_out = N * vs_ub + n_leaf // 2 * V2
     return {
         "external": N * FLOPS["EPS"] + 2 * FLOPS["SPINOR"],
         "propagator_constants": (N + (N if N > 2 else 0)) * FLOPS["MASK"],
@@ -326,13 +326,13 @@ def emit_regs_body1p(N: int, fence: bool = True, inter: bool = False) -> str:
     w("    #pragma unroll")
     w("    for (int i = 0; i < 32; ++i) acc[i] = 0.0;")
     w("    const qed::spinor ub = qed::ubar_spinor(pp, sp);")
-    # s' is the run-time pass index: ubar(p', s') with the zeros common to both spins (ZUX); instantiating
-    # the two passes separately for the full pattern measured 5-10 % slower (code size, sweep_s3_unroll_rejected)
-    zub = "qed::ZUX"
+    # s' is the run-time pass index: the out-side first level branches (warp-uniformly) to the specialisation of
+    # ubar(p', s') for that spin (vs_row_ub, all four zeros skipped; +2.3 %, profiles/ab_s3_ub.jsonl); instantiating
+    # the whole pass per spin instead measured 5-10 % slower (code size, sweep_s3_unroll_rejected)
     for b in range(3):
         for lb in range(2):
             w(f"    {{  // tau_1 = photon {b}, lam_{b} = {lb}")
-            w(f"      const qed::spinor I = qed::vs_row_z<{zub}, {'true' if lb else 'false'}>(mc[{b}], e[{b}][{lb}], ub);")
+            w(f"      const qed::spinor I = qed::vs_row_ub<{'true' if lb else 'false'}>(mc[{b}], e[{b}][{lb}], ub, sp);")
             for c in range(3):
                 if c == b:
                     continue
@@ -444,6 +444,7 @@ def emit_regs_body_bg(N: int = 3) -> str:
 
     def pout(x):
         for lam in range(2):
+            # (the per-spin specialisation of vs_row_ub spills 436 bytes in this body and measured -5.6 %)
             w(f"    P[{x}][{lam}] = qed::vs_row_z<qed::ZUX, {'true' if lam else 'false'}>(mc[{x}], e[{x}][{lam}], ub);")
 
     def block(a_, b, c):

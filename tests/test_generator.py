@@ -208,6 +208,9 @@ def _sparse_call_flops():
             out[f"vs_row_z<qed::{zn}, {tn}>("] = sparse_vs(z, t)
             out[f"eslash_row_z<qed::{zn}, {tn}>("] = sparse_v(z, t)[0]
             out[f"eslash_col_z<qed::{zn}, {tn}>("] = sparse_v(z, t)[0]
+    for t in (False, True):   # vs_row_ub: the spin's own pattern; both spins cost the same
+        assert sparse_vs(ZU[0], t) == sparse_vs(ZU[1], t)
+        out[f"vs_row_ub<{'true' if t else 'false'}>("] = sparse_vs(ZU[0], t)
     return out
 
 
@@ -256,9 +259,9 @@ def test_register_body_flops_match_the_flop_model():
     gen_vs = {False: 40 + 56, True: 24 + 56}
     save_u = sum(gen_vs[lam == 1] - sparse_vs(ZU[s], lam == 1) for s in range(2) for lam in range(2))
     save_ub1 = sum({False: 40, True: 24}[lam == 1] - sparse_v(ZU[s], lam == 1)[0] for s in range(2) for lam in range(2))
-    save_ubx = sum(gen_vs[lam == 1] - sparse_vs(ZUX, lam == 1) for lam in range(2))
+    save_ub = sum(gen_vs[lam == 1] - sparse_vs(ZU[s], lam == 1) for s in range(2) for lam in range(2))
     assert sum(_flops(2).values()) == make_plan(2).flops_per_point - 16 * 8 - 2 * save_u - 2 * save_ub1
-    assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36 - 3 * save_u - 3 * 2 * save_ubx
+    assert sum(_flops(3).values()) == make_plan(3).flops_per_point - 16 * 36 - 3 * save_u - 3 * save_ub
 
 
 def test_sparse_external_patterns_and_generic_counts():
